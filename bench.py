@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: Katz queries/sec at R-MAT scale-22 (BASELINE.json configs[2]).
+
+One step = one batch of b=256 seeded queries through the hot path: batched
+plain-CG Katz solve (tol 1e-8, beta = 0.5/lambda_max) + masked top-100
+(katz_rank semantics).  The R-MAT LRC index is infeasible for the reference
+(SURVEY.md §0.3), so the headline path is the reference's query_cg_baseline
+/ cg recurrence.  Inputs are seeded synthetic graphs (no dataset), and every
+solve vector block (4.9 GB) is far larger than L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
+  python bench.py --impl reference ...   # CPU oracle port of the reference path
+
+Multi-GPU: one process per GPU (torchrun), each rank a full replica solving
+its own 256-query batch (queries are independent columns: weak scaling, no
+collective on the data path); timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Katz queries/sec at R-MAT scale-22, beta=0.5/lambda_max; SpMM HBM GB/s vs peak"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "proxy16", "cfg2", "cfg3"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, smax, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, r[2:]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_graph(cfg):
+    from paper_1912_06525_b200 import generators as G
+
+    spec = G.CONFIGS[cfg]
+    if spec["kind"] == "rmat":
+        return G.rmat_graph_fast(spec["scale"], seed=0)
+    return G.config_graph(cfg)
+
+
+def cpu_sample(g, beta, qs, tol, budget, threads):
+    """The oracle port of query_cg_baseline (reference cg over scipy CSR) on
+    the host cores: solve queries in waves of `threads` until `budget` s."""
+    from oracle import katz_oracle as O
+
+    a = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
+    done = 0
+    iters = []
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        pos = 0
+        while True:
+            wave = [int(q) for q in qs[pos : pos + threads]]
+            if not wave:
+                pos = 0
+                continue
+            res = list(ex.map(lambda q: O.query_cg_csr(a, beta, q, tol=tol), wave))
+            iters += [r[1].iterations for r in res]
+            done += len(wave)
+            pos += len(wave)
+            if time.perf_counter() - t0 >= budget:
+                break
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt, iters
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1912_06525_b200 import generators as G
+
+    spec = G.CONFIGS[args.config]
+    b, k, tol = spec["b"], spec["k"], spec["tol"]
+    workload = {"cfg1": "Chung-Lu n=10^4", "proxy16": "R-MAT scale 16", "cfg2": "R-MAT scale 18",
+                "cfg3": "R-MAT scale 22"}[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, world, rank, spec, workload)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_06525_b200 as kz
+    from paper_1912_06525_b200 import _lib
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+
+    t0 = time.perf_counter()
+    g = build_graph(args.config)
+    t_graph = time.perf_counter() - t0
+    lam = kz.spectral_norm(g)
+    beta = 0.5 / lam
+    idx = kz.GraphIndex(g, beta, spectral_norm=lam)
+    op = idx.operator()
+    qs = G.sample_queries(g.original_ids, b, seed=rank)
+    internal = idx.internal_ids(qs)
+    n, nnz = g.n, g.nnz
+
+    def step():
+        scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol, device=True)
+        ids, vals, counts = kz.topk_device(scores, k, idx.mask_operator(), internal, internal)
+        return reps, ids
+
+    for _ in range(args.warmup):
+        reps, _ = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = lib.kz_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    iters_all = []
+    solve_ms = 0.0
+    for _ in range(args.steps):
+        reps, _ = step()
+        iters_all.append([r.iterations for r in reps])
+        solve_ms += reps[0].wall_time * 1e3
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = lib.kz_launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    clock_info = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = b * world / (ms / 1e3)
+
+    # ---- e2e: public API with host buffers (H2D queries, D2H ranked lists) ----
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t1 = time.perf_counter()
+        preds = kz.katz_rank_batch(idx, qs, k, tol=tol)
+        e2e_t.append(time.perf_counter() - t1)
+    e2e_s = statistics.median(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    mean_iters = float(np.mean(iters_all))
+    h2d = 3 * 8 * b  # qpos, mask rows, self ids (int64)
+    d2h = b * k * 16 + b * 4 + b * 32 + 8 * int(np.max(iters_all) + 2)
+
+    # ---- roofline of the dominant kernel: the K1 SpMM of one CG iteration ----
+    C = 16 if b >= 16 else 1
+    nch = (b + C - 1) // C
+    X = torch.randn(nch * C * n, dtype=torch.float64, device="cuda")
+    Y = torch.empty_like(X)
+    dots = torch.empty(nch * C, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        op.spmm(X, Y, b=nch * C, chunk=C, Xs=X, s1=1.0, s2=-beta, dots=dots)
+    reps_spmm = 5
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps_spmm):
+        op.spmm(X, Y, b=nch * C, chunk=C, Xs=X, s1=1.0, s2=-beta, dots=dots)
+    e1.record()
+    torch.cuda.synchronize()
+    spmm_ms = e0.elapsed_time(e1) / reps_spmm
+    del X, Y
+    blk = 8.0 * n * b
+    b_spmm = 4.0 * nnz + 4.0 * (n + 1) + 2 * blk
+    b_cg = 4.0 * nnz + 4.0 * (n + 1) + 10 * blk  # spmm(2) + update(3) + pupdate(5) blocks
+    peak, peak_src = peaks()
+    achieved = b_spmm / (spmm_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(prof):
+        traffic = json.load(open(prof)).get("spmm_dram_bytes_per_launch")
+    cg_iter_ms = solve_ms / args.steps / max(1.0, float(np.max(iters_all)))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        qps, done, dt, it = cpu_sample(g, beta, qs, tol, args.cpu_budget, threads)
+        cpu = {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
+               "sample": f"{done} of the {b} bench queries ({workload}), oracle CSR cg "
+                         f"(reference solver.py:62-101 recurrence) on {threads} host threads, {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "queries/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
+            "config": {"workload": workload, "n": n, "nnz": nnz, "beta": beta, "lambda_max": lam,
+                       "queries_per_gpu": b, "top_k": k, "tol": tol, "solver": "plain CG (query_cg_baseline)",
+                       "mean_cg_iterations": mean_iters, "l2": "inputs larger than L2 (4.9 GB blocks), no flush",
+                       "parallelism": f"replicas x{world} (query-column sharding)",
+                       "graph_build_s": round(t_graph, 1)},
+            "e2e": {"value": b * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "api": "paper_1912_06525_b200.katz_rank_batch (host ids in, host ranked lists out)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": f"spmm_kernel<{C}>",
+                         "algorithmic_bytes_per_launch": b_spmm, "launch_ms": spmm_ms,
+                         "peak_source": peak_src,
+                         "cg_iteration": {"algorithmic_bytes": b_cg, "ms": cg_iter_ms,
+                                          "achieved_gbs": b_cg / (cg_iter_ms / 1e3) / 1e9}},
+            "cpu_baseline": cpu,
+            "clocks": clock_info,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank, spec, workload):
+    """--impl reference: the reference's CPU path (oracle port of cg over
+    scipy CSR, fanned out over host threads like cli.py:105-112)."""
+    if rank != 0:
+        return
+    from paper_1912_06525_b200 import generators as G
+
+    g = build_graph(args.config)
+    try:
+        import paper_1912_06525_b200 as kz
+
+        lam = kz.spectral_norm(g)  # input preparation only (beta); not timed
+    except Exception:
+        from oracle import katz_oracle as O
+        import scipy.sparse.linalg as sla
+
+        a = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
+        lam = float(abs(sla.eigsh(a, k=1, which="LM", return_eigenvectors=False)[0]))
+    beta = 0.5 / lam
+    b, tol = spec["b"], spec["tol"]
+    qs = G.sample_queries(g.original_ids, b, seed=0)
+    threads = len(os.sched_getaffinity(0))
+    per_step_budget = max(5.0, 150.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_sample(g, beta, qs, tol, 0.0, threads)
+    vals = []
+    total, total_t = 0, 0.0
+    for _ in range(args.steps):
+        qps, done, dt, _ = cpu_sample(g, beta, qs, tol, per_step_budget, threads)
+        vals.append(qps)
+        total += done
+        total_t += dt
+    value = total / total_t
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md Appendix B)", "impl": "reference",
+        "config": {"workload": workload, "n": g.n, "nnz": g.nnz, "beta": beta, "queries_per_gpu": b,
+                   "top_k": spec["k"], "tol": tol, "solver": "plain CG (query_cg_baseline)"},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": f"{total} queries of the {b}-query batch in waves of {threads}"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * katzb200.h -- C-ABI of the B200-native Katz query hot path (libkatzb200.so).
+ *
+ * This is the drop-in boundary for the query path of the reference package
+ * `lrckatz` (/root/reference/pkg/src/lrckatz).  The reference has no FFI: its
+ * boundary is the module-level Python API re-exported in __init__.py:9-72.
+ * Each entry point below replaces the numpy/scipy arithmetic behind one of
+ * those Python functions; the Python mirror in paper_1912_06525_b200/ binds
+ * them through ctypes.
+ *
+ * Conventions
+ *  - Every function returns an int status (KZ_OK == 0).  On failure
+ *    kz_last_error() returns a thread-local message.
+ *  - Device pointers are plain CUDA device pointers (e.g. torch tensors'
+ *    data_ptr()); `stream` is a cudaStream_t passed as void*.
+ *  - Dense blocks of b vectors of length n use the "chunked node-major"
+ *    layout [b/C][n][C]: element (row i, column j) lives at
+ *    ((j / C) * n + i) * C + (j % C).  C == 1 is plain column-major [b][n].
+ *  - All arithmetic is IEEE fp64.  Indices are int32 on the device
+ *    (nnz < 2^31 is checked at creation).
+ *  - Handles are immutable after creation; calls on distinct streams with
+ *    distinct workspaces are reentrant (reference SPEC.md:359 threading).
+ */
+#ifndef KATZB200_H
+#define KATZB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python mirror maps them to the reference exceptions */
+#define KZ_OK 0
+#define KZ_EARG 1      /* ValueError            (solver.py:106-107, linkpred.py:157-181) */
+#define KZ_ENOTSPD 2   /* RuntimeError "... not positive definite" (solver.py:84-85,140-141) */
+#define KZ_ESPECTRUM 3 /* SpectrumError         (factor.py:27-28,329-330) */
+#define KZ_ECUDA 4     /* RuntimeError (CUDA failure) */
+#define KZ_EOOM 5      /* MemoryError */
+
+/* Binary-pattern CSR operator A (rows x cols, no stored values) resident on
+ * the device, plus its precomputed SpMM schedule (row partition, long-row
+ * segments).  Replaces the scipy CSR operands of solver.py:110,115,178 and
+ * index.py:89-90. */
+typedef struct kz_graph kz_graph;
+
+/* Per-query solve report; mirrors SolveReport (solver.py:29-34). */
+typedef struct kz_report {
+    int64_t iterations;
+    int32_t converged;
+    int32_t status; /* per-column KZ_* status (KZ_ENOTSPD for p.q <= 0) */
+    double final_residual_norm;
+    double rhs_norm;
+} kz_report;
+
+const char* kz_last_error(void);
+int kz_version(void);
+/* total kernels this library has launched in the process (bench evidence) */
+long long kz_launch_count(void);
+
+/* ---- operator handles ------------------------------------------------- */
+
+/* Upload a CSR pattern.  rowptr: int64[rows+1], colidx: int32[nnz]; either
+ * host or device memory (UVA-detected).  Columns must lie in [0, cols). */
+int kz_graph_create(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
+                    const int32_t* colidx, kz_graph** out);
+int kz_graph_destroy(kz_graph* g);
+/* rows, cols, nnz, number of long rows, number of long-row segments */
+int kz_graph_info(const kz_graph* g, int64_t* rows, int64_t* cols, int64_t* nnz,
+                  int64_t* nlong, int64_t* nitems);
+
+/* ---- K1: binary CSR SpMM with fused epilogue ---------------------------
+ * Y = s0*Z + s1*Xs + s2*(A Xg)  on b columns in layout [b/C][.][C];
+ * Xg has `cols` rows, Xs/Z/Y/D have `rows` rows.  Z or Xs may be NULL.
+ * If dots != NULL (device double[b]) it receives dots[j] = sum_i D[i,j]*Y[i,j]
+ * (D == NULL means D = Xs).  Replaces KatzIndex.apply_m_permuted
+ * (index.py:86-91) with s0=0, s1=1, s2=-alpha, and the m12 / m12.T products
+ * of solver.py:110,115,178.  Workspace: kz_spmm_workspace_bytes(). */
+size_t kz_spmm_workspace_bytes(const kz_graph* g, int32_t b, int32_t chunk);
+int kz_spmm(const kz_graph* g, int32_t b, int32_t chunk, const double* Xg, const double* Xs,
+            const double* Z, double* Y, double s0, double s1, double s2, const double* D,
+            double* dots, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K2: batched textbook CG on (I - beta*A) x = rhs --------------------
+ * One call solves b Katz queries (columns) with per-column convergence
+ * masking; each column follows cg() (solver.py:62-101) exactly: x0 = 0 (or
+ * the given start vector), stop when ||r|| <= tol*||rhs||, raise (KZ_ENOTSPD)
+ * if p.q <= 0, at most max_iter iterations.  The right-hand side of column j
+ * is beta * A[:, qpos[j]] (rhs_for_position, index.py:93-101) unless `rhs`
+ * is given.  Output: scores[j][perm[i]] = clamp(x_j[i]) (solver.py:223-225). */
+typedef struct kz_cg_args {
+    int32_t b;            /* number of query columns */
+    int32_t clamp;        /* 1: scores = max(x, 0) */
+    const int64_t* qpos;  /* host int64[b]: query rows (operator order); ignored if rhs */
+    const double* rhs;    /* device double[b][n] column-major, or NULL */
+    double beta;          /* damping factor (alpha of the reference) */
+    double tol;           /* relative residual tolerance */
+    int64_t max_iter;     /* <= 0 means 10*n (solver.py:69-70) */
+    const double* x0;     /* device double[n] start vector shared by all columns, or NULL */
+    const int64_t* perm;  /* device int64[n] output scatter (perm[i] = internal id), or NULL */
+    double* scores;       /* device double[b][n] output */
+    kz_report* reports;   /* host kz_report[b] output */
+    float* device_ms;     /* optional host float: device time of the solve (CUDA events) */
+} kz_cg_args;
+size_t kz_cg_workspace_bytes(const kz_graph* g, int32_t b);
+int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K4: batched masked top-k --------------------------------------------
+ * For each column j of scores (device double[b][n], entries >= 0) select the
+ * k entries with the largest (score desc, id asc) key among ids that are not
+ * masked.  The mask of column j is {self_ids[j]} U neighbors(mask_rows[j]) in
+ * mask_graph (either part may be -1 / NULL).  This is _candidate_order
+ * (linkpred.py:145-152) and the anchor selection (linkpred.py:186-188).
+ * Outputs: ids_out int64[b][k], vals_out double[b][k], count_out int32[b]. */
+typedef struct kz_topk_args {
+    int32_t b;
+    int32_t k;
+    int64_t n;
+    const double* scores;
+    const kz_graph* mask_graph; /* may be NULL */
+    const int64_t* mask_rows;   /* host int64[b] or NULL */
+    const int64_t* self_ids;    /* host int64[b] or NULL */
+    int64_t* ids_out;
+    double* vals_out;
+    int32_t* count_out;
+} kz_topk_args;
+size_t kz_topk_workspace_bytes(int32_t b, int64_t n, int32_t k);
+int kz_topk_batch(const kz_topk_args* a, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K7: sparse_katz anchor profiles and Pearson rerank ------------------
+ * kz_profile_gather: for each triple t = (src, j, slot) of trip (device
+ * int64[ntrip][3]) copy S[src][top_ids[j][c]] into profiles[j][slot][c] for
+ * c < counts[j]  (the profile rows of linkpred.py:189-196).
+ * kz_pearson_rerank: per query j, corr[c] = Pearson(ref[j], profiles[j][:, c])
+ * (0 for zero variance, clipped to [-1, 1]) and the rerank order of
+ * lexsort((top, -score, -corr)) (linkpred.py:197-205).  s <= 2048. */
+int kz_profile_gather(const double* S, int64_t n, int32_t ntrip, const int64_t* trip,
+                      const int64_t* top_ids, const int32_t* counts, int32_t s, double* profiles,
+                      int32_t T1, void* stream);
+int kz_pearson_rerank(const double* profiles, const double* ref, const int64_t* top_ids,
+                      const double* top_scores, const int32_t* counts, int32_t b, int32_t T1,
+                      int32_t s, double* corr_out, int64_t* order_out, void* stream);
+
+/* ---- vector helpers used by the generic cg() / lrc_pcg() drivers -------- */
+/* out[j] = sum_i X[i,j]*Y[i,j] over b columns of length n (column-major). */
+int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KATZB200_H */

@@ -1,0 +1,67 @@
+"""B200-native Katz query hot path with the API of the reference ``lrckatz``.
+
+Drop-in for the query side of lrckatz (reference __init__.py:9-72): load a
+KLRC index built by the reference and answer ``query`` (LRC-Katz Schur
+PCG), ``query_cg_baseline`` (plain CG), ``katz_rank`` and ``sparse_katz``
+on one GPU through libkatzb200.so (hand-written sm_100a kernels).  Batched
+variants (``*_batch``) solve many queries per device call.  The offline
+index build, partitioner, recall harness and CLI of the reference are out
+of scope.
+"""
+
+from .factor import (
+    BlockCholesky,
+    DenseCholesky,
+    FactorizationError,
+    LowRankCorrection,
+    SpectrumError,
+)
+from .graph import (
+    ConvergenceError,
+    DeviceOperator,
+    Graph,
+    GraphParseError,
+    InadmissibleAlphaError,
+    KatzParams,
+    from_edges,
+    hardest_alpha,
+    largest_connected_component,
+    spectral_norm,
+)
+from .index import (
+    FORMAT_VERSION,
+    BlockPartition,
+    GraphIndex,
+    IndexChecksumError,
+    IndexFormatError,
+    IndexMagicError,
+    IndexVersionError,
+    KatzIndex,
+    load_index,
+    save_index,
+)
+from .linkpred import (
+    RankedPrediction,
+    katz_rank,
+    katz_rank_batch,
+    pearson,
+    sparse_katz,
+    sparse_katz_batch,
+    topk_device,
+)
+from .solver import (
+    KatzOperator,
+    KatzVector,
+    SolveReport,
+    UnknownNodeError,
+    apply_schur,
+    cg,
+    lrc_pcg,
+    query,
+    query_batch,
+    query_cg_baseline,
+    query_cg_baseline_batch,
+    schur_rhs,
+)
+
+__version__ = "0.1.0"

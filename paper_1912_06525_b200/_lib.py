@@ -1,0 +1,235 @@
+"""ctypes binding of libkatzb200.so (the C-ABI declared in include/katzb200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_1912_06525_b200/csrc``).  There is no fallback: if the
+library or a CUDA device is missing, every device entry point raises
+``KatzDeviceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkatzb200.so")
+
+KZ_OK = 0
+KZ_EARG = 1
+KZ_ENOTSPD = 2
+KZ_ESPECTRUM = 3
+KZ_ECUDA = 4
+KZ_EOOM = 5
+
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "katzb200.h")
+
+
+def header_symbols(path=HEADER_PATH):
+    """Names of the functions include/katzb200.h declares."""
+    import re
+
+    text = open(path).read()
+    text = re.sub(r"/\*.*?\*/", " ", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(kz_[a-z0-9_]+)\s*\(", text)))
+
+
+class KatzDeviceError(RuntimeError):
+    """The CUDA extension or the GPU is unavailable (there is no CPU path)."""
+
+
+class KzReport(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int64),
+        ("converged", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("final_residual_norm", ctypes.c_double),
+        ("rhs_norm", ctypes.c_double),
+    ]
+
+
+class KzCgArgs(ctypes.Structure):
+    _fields_ = [
+        ("b", ctypes.c_int32),
+        ("clamp", ctypes.c_int32),
+        ("qpos", ctypes.POINTER(ctypes.c_int64)),
+        ("rhs", ctypes.c_void_p),
+        ("beta", ctypes.c_double),
+        ("tol", ctypes.c_double),
+        ("max_iter", ctypes.c_int64),
+        ("x0", ctypes.c_void_p),
+        ("perm", ctypes.c_void_p),
+        ("scores", ctypes.c_void_p),
+        ("reports", ctypes.POINTER(KzReport)),
+        ("device_ms", ctypes.POINTER(ctypes.c_float)),
+    ]
+
+
+class KzTopkArgs(ctypes.Structure):
+    _fields_ = [
+        ("b", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("n", ctypes.c_int64),
+        ("scores", ctypes.c_void_p),
+        ("mask_graph", ctypes.c_void_p),
+        ("mask_rows", ctypes.POINTER(ctypes.c_int64)),
+        ("self_ids", ctypes.POINTER(ctypes.c_int64)),
+        ("ids_out", ctypes.c_void_p),
+        ("vals_out", ctypes.c_void_p),
+        ("count_out", ctypes.c_void_p),
+    ]
+
+
+class KzLrcDesc(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("n1", ctypes.c_int64),
+        ("n2", ctypes.c_int64),
+        ("ell", ctypes.c_int64),
+        ("beta", ctypes.c_double),
+        ("a_rowptr", ctypes.c_void_p),
+        ("a_colidx", ctypes.c_void_p),
+        ("a_nnz", ctypes.c_int64),
+        ("num_parts", ctypes.c_int64),
+        ("part_ptr", ctypes.c_void_p),
+        ("part_inv", ctypes.c_void_p),
+        ("part_inv_off", ctypes.c_void_p),
+        ("linv", ctypes.c_void_p),
+        ("u", ctypes.c_void_p),
+        ("sigma", ctypes.c_void_p),
+    ]
+
+
+class KzLrcArgs(ctypes.Structure):
+    _fields_ = [
+        ("b", ctypes.c_int32),
+        ("clamp", ctypes.c_int32),
+        ("qpos", ctypes.POINTER(ctypes.c_int64)),
+        ("tol", ctypes.c_double),
+        ("max_iter", ctypes.c_int64),
+        ("x0", ctypes.c_void_p),
+        ("perm", ctypes.c_void_p),
+        ("scores", ctypes.c_void_p),
+        ("reports", ctypes.POINTER(KzReport)),
+        ("device_ms", ctypes.POINTER(ctypes.c_float)),
+    ]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(require=True):
+    """Load libkatzb200.so once; raises KatzDeviceError if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            if require:
+                raise KatzDeviceError(
+                    f"{LIB_PATH} is missing; build it with __graft_entry__.build() "
+                    "(there is no CPU fallback)"
+                )
+            return None
+        lib = ctypes.CDLL(LIB_PATH)
+        _declare(lib)
+        _lib = lib
+        return lib
+
+
+def _declare(lib):
+    c = ctypes
+    vp, i32, i64, dbl, sz = c.c_void_p, c.c_int32, c.c_int64, c.c_double, c.c_size_t
+    lib.kz_last_error.restype = c.c_char_p
+    lib.kz_version.restype = c.c_int
+    lib.kz_launch_count.restype = c.c_longlong
+    lib.kz_graph_create.argtypes = [i64, i64, i64, vp, vp, c.POINTER(vp)]
+    lib.kz_graph_destroy.argtypes = [vp]
+    lib.kz_graph_info.argtypes = [vp] + [c.POINTER(i64)] * 5
+    lib.kz_spmm_workspace_bytes.argtypes = [vp, i32, i32]
+    lib.kz_spmm_workspace_bytes.restype = sz
+    lib.kz_spmm.argtypes = [vp, i32, i32, vp, vp, vp, vp, dbl, dbl, dbl, vp, vp, vp, sz, vp]
+    lib.kz_cg_workspace_bytes.argtypes = [vp, i32]
+    lib.kz_cg_workspace_bytes.restype = sz
+    lib.kz_cg_batch.argtypes = [vp, c.POINTER(KzCgArgs), vp, sz, vp]
+    lib.kz_topk_workspace_bytes.argtypes = [i32, i64, i32]
+    lib.kz_topk_workspace_bytes.restype = sz
+    lib.kz_topk_batch.argtypes = [c.POINTER(KzTopkArgs), vp, sz, vp]
+    lib.kz_coldot.argtypes = [i64, i32, vp, vp, vp, vp]
+    lib.kz_profile_gather.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp, i32, vp]
+    lib.kz_pearson_rerank.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp]
+    if hasattr(lib, "kz_lrc_create"):
+        lib.kz_lrc_create.argtypes = [c.POINTER(KzLrcDesc), c.POINTER(vp)]
+        lib.kz_lrc_destroy.argtypes = [vp]
+        lib.kz_lrc_info.argtypes = [vp, c.POINTER(i64), c.POINTER(i64), c.POINTER(i64), c.POINTER(i64)]
+        lib.kz_lrc_workspace_bytes.argtypes = [vp, i32]
+        lib.kz_lrc_workspace_bytes.restype = sz
+        lib.kz_lrc_batch.argtypes = [vp, c.POINTER(KzLrcArgs), vp, sz, vp]
+        lib.kz_lrc_apply_schur.argtypes = [vp, i32, vp, vp, vp, sz, vp]
+        lib.kz_lrc_apply_precond.argtypes = [vp, i32, vp, vp, vp, sz, vp]
+        lib.kz_lrc_schur_rhs.argtypes = [vp, i32, vp, vp, vp, vp, sz, vp]
+        lib.kz_dense_matmul.argtypes = [i64, i64, i64, dbl, vp, i64, i32, vp, i64, i32, dbl, vp, i64, i32, vp]
+
+
+def error_from_status(code, lib=None):
+    """Map a KZ_* status to the reference's exception types."""
+    lib = lib or _lib
+    msg = lib.kz_last_error().decode() if lib is not None else ""
+    if code == KZ_EARG:
+        return ValueError(msg)
+    if code == KZ_ENOTSPD:
+        return RuntimeError(msg or "operator is not positive definite")
+    if code == KZ_ESPECTRUM:
+        from .factor import SpectrumError
+
+        return SpectrumError(msg)
+    if code == KZ_EOOM:
+        return MemoryError(msg)
+    return KatzDeviceError(msg or f"CUDA failure (status {code})")
+
+
+def check(code):
+    if code != KZ_OK:
+        raise error_from_status(code)
+
+
+def torch_cuda():
+    """Import torch and insist on a CUDA device (no CPU fallback)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise KatzDeviceError("no CUDA device: the B200 query path has no CPU fallback")
+    return torch
+
+
+def stream_ptr(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def i64_array(values):
+    arr = np.ascontiguousarray(values, dtype=np.int64)
+    return arr, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+class Workspace:
+    """Per-thread cache of device scratch buffers (grown on demand)."""
+
+    _tls = threading.local()
+
+    @classmethod
+    def get(cls, torch, nbytes, slot="default"):
+        cache = getattr(cls._tls, "cache", None)
+        if cache is None:
+            cache = cls._tls.cache = {}
+        buf = cache.get(slot)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
+            cache[slot] = buf
+        return buf

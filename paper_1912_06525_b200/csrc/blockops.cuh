@@ -1,0 +1,403 @@
+// blockops.cuh -- streaming kernels over chunked blocks [b/C][rows][C]:
+// deterministic column dots with a per-chunk finalize hook, the fused CG
+// vector updates, layout transposes in/out.  Shared by the CG (cg.cu) and
+// the LRC Schur-PCG (lrc.cu) drivers.
+#pragma once
+
+#include "spmm.cuh"
+
+namespace kz {
+
+// Per-column solver state (device arrays of length bpad unless noted).
+struct SolveState {
+    int32_t b = 0, bpad = 0, C = 0, nchunks = 0;
+    int64_t rows = 0;
+    int64_t max_iter = 0;
+    double tol = 0.0;
+    double* rs = nullptr;      // r.r (CG) / r.z (PCG)
+    double* alpha = nullptr;   // step length of the current iteration
+    double* betac = nullptr;   // direction update coefficient
+    double* thresh = nullptr;  // tol * ||b||
+    double* rnorm = nullptr;   // ||r|| (recursive)
+    double* bnorm2 = nullptr;  // ||b||^2
+    double* rr = nullptr;      // scratch: r.r of the current iteration (PCG)
+    int64_t* iters = nullptr;
+    int32_t* active = nullptr;
+    int32_t* xstamp = nullptr;
+    int32_t* status = nullptr;
+    int32_t* converged = nullptr;
+    int32_t* chunk_active = nullptr;  // [nchunks]
+    int32_t* chunk_xstamp = nullptr;  // [nchunks]
+    int32_t* n_active = nullptr;      // [1]
+    int32_t* err = nullptr;           // [1]
+};
+
+enum FinalizeMode : int {
+    FIN_WRITE = 0,      // out[col] = v
+    FIN_INIT_B = 1,     // bnorm2 = v
+    FIN_INIT_BR = 2,    // bnorm2 = v and r == b: run init finalize
+    FIN_INIT_R = 3,     // v = r.r after a start vector: run init finalize
+    FIN_CG_CONV = 4,    // v = r.r after the update: convergence test (cg)
+    FIN_PCG_RR = 5,     // v = r.r after the update: store, test convergence (pcg)
+    FIN_PCG_RZ = 6,     // v = r.z: direction coefficient (pcg)
+    FIN_PCG_INIT_RZ = 7 // v = r.z at start: rs = v (pcg)
+};
+
+// init finalize shared by cg() and lrc_pcg(): solver.py:71-77 / 127-133
+__device__ __forceinline__ bool init_finalize(const SolveState& s, int col, double rr) {
+    const double bn = sqrt(s.bnorm2[col]);
+    s.thresh[col] = s.tol * bn;
+    const double rn = sqrt(rr);
+    s.rnorm[col] = rn;
+    s.rs[col] = rr;
+    s.iters[col] = 0;
+    const bool act = rn > s.thresh[col];
+    s.active[col] = act ? 1 : 0;
+    s.converged[col] = act ? 0 : 1;
+    if (act) atomicAdd(s.n_active, 1);
+    return act;
+}
+
+// Applies the finalize of `mode` for the C columns of `chunk`; run by the
+// last CTA of the chunk with v valid in threads < C.  Returns nothing; keeps
+// chunk_active in sync.
+template <int C>
+__device__ __forceinline__ void finalize_chunk(int mode, const SolveState& s, double* out,
+                                               int chunk, int iter, double v) {
+    const int col = chunk * C + threadIdx.x;
+    bool act = false;
+    if (threadIdx.x < C) {
+        if (mode == FIN_WRITE) {
+            if (out) out[col] = v;
+        } else if (col >= s.b) {
+            act = false;
+        } else if (mode == FIN_INIT_B) {
+            s.bnorm2[col] = v;
+        } else if (mode == FIN_INIT_BR) {
+            s.bnorm2[col] = v;
+            act = init_finalize(s, col, v);
+        } else if (mode == FIN_INIT_R) {
+            act = init_finalize(s, col, v);
+        } else if (mode == FIN_CG_CONV) {
+            // solver.py:89-95
+            if (s.xstamp[col] == iter && s.active[col]) {
+                const int64_t it = s.iters[col] + 1;
+                s.iters[col] = it;
+                const double rn = sqrt(v);
+                s.rnorm[col] = rn;
+                if (rn <= s.thresh[col]) {
+                    s.active[col] = 0;
+                    s.converged[col] = 1;
+                    atomicSub(s.n_active, 1);
+                } else if (it >= s.max_iter) {
+                    s.active[col] = 0;
+                    atomicSub(s.n_active, 1);
+                } else {
+                    s.betac[col] = v / s.rs[col];
+                    s.rs[col] = v;
+                }
+            }
+            act = s.active[col] != 0;
+        } else if (mode == FIN_PCG_RR) {
+            // solver.py:145-148 (norm of r, stop test)
+            if (s.xstamp[col] == iter && s.active[col]) {
+                const int64_t it = s.iters[col] + 1;
+                s.iters[col] = it;
+                const double rn = sqrt(v);
+                s.rnorm[col] = rn;
+                if (rn <= s.thresh[col]) {
+                    s.active[col] = 0;
+                    s.converged[col] = 1;
+                    atomicSub(s.n_active, 1);
+                } else if (it >= s.max_iter) {
+                    s.active[col] = 0;
+                    atomicSub(s.n_active, 1);
+                }
+            }
+            act = s.active[col] != 0;
+        } else if (mode == FIN_PCG_RZ) {
+            // solver.py:150-152
+            if (s.active[col]) {
+                s.betac[col] = v / s.rs[col];
+                s.rs[col] = v;
+            }
+            act = s.active[col] != 0;
+        } else if (mode == FIN_PCG_INIT_RZ) {
+            if (s.active[col]) s.rs[col] = v;
+            act = s.active[col] != 0;
+        }
+    }
+    if (mode != FIN_WRITE && mode != FIN_INIT_B && s.chunk_active) {
+        const int any = __syncthreads_or(act ? 1 : 0);
+        if (threadIdx.x == 0) s.chunk_active[chunk] = any;
+    }
+}
+
+// Reduce per-thread column values (thread owns columns ((tid*VEC)%C)+q) to
+// one value per column in threads < C.  sm: kThreads doubles.
+template <int C, int VEC>
+__device__ __forceinline__ double block_col_reduce(double (&v)[VEC], double* sm) {
+    constexpr int G = C / VEC;  // lanes covering one row segment of C columns
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = G; off < 32; off <<= 1)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+    if (lane < G) {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) sm[warp * C + lane * VEC + q] = v[q];
+    }
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < C)
+        for (int w = 0; w < kWarps; ++w) s += sm[w * C + threadIdx.x];
+    __syncthreads();
+    return s;
+}
+
+struct RedScratch {
+    double* part = nullptr;   // [nchunks][nb][C]
+    int32_t* cnt = nullptr;   // [nchunks]
+    int nb = 1;               // CTAs per chunk
+};
+
+// Last-CTA-of-chunk protocol: write this CTA's partial, count, and return
+// true (with the fixed-order total in threads < C) in the last CTA.
+template <int C>
+__device__ __forceinline__ bool chunk_last_reduce(const RedScratch& rs, int chunk, int local,
+                                                  double mine, double* sm, double& total) {
+    __shared__ int is_last;
+    if (threadIdx.x < C) {
+        rs.part[(static_cast<size_t>(chunk) * rs.nb + local) * C + threadIdx.x] = mine;
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(rs.cnt + chunk, 1) == rs.nb - 1);
+    __syncthreads();
+    if (!is_last) return false;
+    __threadfence();
+    total = reduce_partials<C>(rs.part + static_cast<size_t>(chunk) * rs.nb * C, rs.nb, sm);
+    if (threadIdx.x == 0) rs.cnt[chunk] = 0;
+    return true;
+}
+
+// out/hook = column dots X.Y over a chunked block.
+template <int C>
+__global__ void __launch_bounds__(kThreads)
+    coldot_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows,
+                  RedScratch red, int mode, SolveState s, double* out, int iter) {
+    constexpr int VEC = Cfg<C>::VEC;
+    const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
+    const size_t base = static_cast<size_t>(chunk) * rows * C;
+    const size_t npairs = static_cast<size_t>(rows) * C / VEC;
+    const size_t stride = static_cast<size_t>(red.nb) * kThreads;
+    double acc[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+    for (size_t pi = static_cast<size_t>(local) * kThreads + threadIdx.x; pi < npairs; pi += stride) {
+        double x[VEC], y[VEC];
+        ld_plain<VEC>(X + base + pi * VEC, x);
+        ld_plain<VEC>(Y + base + pi * VEC, y);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] = fma(x[q], y[q], acc[q]);
+    }
+    __shared__ double sm[kThreads];
+    const double mine = block_col_reduce<C, VEC>(acc, sm);
+    double total;
+    if (chunk_last_reduce<C>(red, chunk, local, mine, sm, total))
+        finalize_chunk<C>(mode, s, out, chunk, iter, total);
+}
+
+// CG residual update (solver.py:88-90) fused with r.r:  r -= a*q for the
+// columns active in this iteration.
+template <int C>
+__global__ void __launch_bounds__(kThreads)
+    cg_update_kernel(double* __restrict__ r, const double* __restrict__ q, int64_t rows,
+                     RedScratch red, int mode, SolveState s, int iter) {
+    constexpr int VEC = Cfg<C>::VEC;
+    const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
+    if (s.chunk_xstamp[chunk] != iter) return;
+    const size_t base = static_cast<size_t>(chunk) * rows * C;
+    const size_t npairs = static_cast<size_t>(rows) * C / VEC;
+    const size_t stride = static_cast<size_t>(red.nb) * kThreads;
+    const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
+    const int c0 = static_cast<int>((t0 * VEC) % C);  // fixed column of this thread
+    double a[VEC];
+    bool on[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+        const int col = chunk * C + c0 + q;
+        on[q] = col < s.b && s.xstamp[col] == iter;
+        a[q] = on[q] ? s.alpha[col] : 0.0;
+    }
+    double acc[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+    for (size_t pi = t0; pi < npairs; pi += stride) {
+        double rv[VEC], qv[VEC];
+        ld_plain<VEC>(r + base + pi * VEC, rv);
+        ld_plain<VEC>(q + base + pi * VEC, qv);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            if (on[k]) rv[k] = __dsub_rn(rv[k], __dmul_rn(a[k], qv[k]));
+            acc[k] = fma(rv[k], rv[k], acc[k]);
+        }
+        st_plain<VEC>(r + base + pi * VEC, rv);
+    }
+    __shared__ double sm[kThreads];
+    const double mine = block_col_reduce<C, VEC>(acc, sm);
+    double total;
+    if (chunk_last_reduce<C>(red, chunk, local, mine, sm, total))
+        finalize_chunk<C>(mode, s, nullptr, chunk, iter, total);
+}
+
+// Deferred solution update and new direction (solver.py:87, 95 / 144, 151):
+//   x += a*p   for columns active in this iteration
+//   p  = d + betac*p  for columns still active   (d = r for CG, z for PCG)
+template <int C>
+__global__ void __launch_bounds__(kThreads)
+    cg_pupdate_kernel(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ d,
+                      int64_t rows, int nb, SolveState s, int iter) {
+    constexpr int VEC = Cfg<C>::VEC;
+    const int chunk = blockIdx.x / nb, local = blockIdx.x - chunk * nb;
+    if (s.chunk_xstamp[chunk] != iter) return;
+    const size_t base = static_cast<size_t>(chunk) * rows * C;
+    const size_t npairs = static_cast<size_t>(rows) * C / VEC;
+    const size_t stride = static_cast<size_t>(nb) * kThreads;
+    const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
+    const int c0 = static_cast<int>((t0 * VEC) % C);
+    double a[VEC], bc[VEC];
+    bool ox[VEC], op[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+        const int col = chunk * C + c0 + q;
+        ox[q] = col < s.b && s.xstamp[col] == iter;
+        op[q] = ox[q] && s.active[col];
+        a[q] = ox[q] ? s.alpha[col] : 0.0;
+        bc[q] = op[q] ? s.betac[col] : 0.0;
+    }
+    for (size_t pi = t0; pi < npairs; pi += stride) {
+        double xv[VEC], pv[VEC], dv[VEC];
+        ld_plain<VEC>(x + base + pi * VEC, xv);
+        ld_plain<VEC>(p + base + pi * VEC, pv);
+        ld_plain<VEC>(d + base + pi * VEC, dv);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            if (ox[k]) xv[k] = __dadd_rn(xv[k], __dmul_rn(a[k], pv[k]));
+            if (op[k]) pv[k] = __dadd_rn(dv[k], __dmul_rn(bc[k], pv[k]));
+        }
+        st_plain<VEC>(x + base + pi * VEC, xv);
+        st_plain<VEC>(p + base + pi * VEC, pv);
+    }
+}
+
+// rhs of query column j: beta * A[:, qpos[j]] (index.py:93-101), written into
+// a zeroed block.  One CTA per column walks CSR row qpos[j] (A symmetric).
+template <int C>
+__global__ void scatter_rhs_kernel(double* __restrict__ r, int64_t rows,
+                                   const int32_t* __restrict__ rowptr,
+                                   const int32_t* __restrict__ colidx,
+                                   const int64_t* __restrict__ qpos, int b, double beta) {
+    const int j = blockIdx.x;
+    if (j >= b) return;
+    const int64_t q = qpos[j];
+    const int beg = rowptr[q], end = rowptr[q + 1];
+    for (int k = beg + threadIdx.x; k < end; k += blockDim.x)
+        r[blk_index(rows, C, colidx[k], j)] = beta;
+}
+
+// column-major [b][rows] -> chunked block (tile transpose through shared memory)
+template <int C>
+__global__ void load_colmajor_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                     int64_t rows, int b, int nchunks) {
+    constexpr int TR = 64;
+    __shared__ double sm[TR * (C + 1)];
+    const int64_t ntiles = (rows + TR - 1) / TR;
+    for (int64_t t = blockIdx.x; t < ntiles * nchunks; t += gridDim.x) {
+        const int chunk = static_cast<int>(t / ntiles);
+        const int64_t r0 = (t - static_cast<int64_t>(chunk) * ntiles) * TR;
+        for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
+            const int c = e / TR, rr = e % TR;
+            const int col = chunk * C + c;
+            const int64_t row = r0 + rr;
+            sm[rr * (C + 1) + c] = (col < b && row < rows) ? src[static_cast<size_t>(col) * rows + row] : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
+            const int rr = e / C, c = e % C;
+            const int64_t row = r0 + rr;
+            if (row < rows) dst[(static_cast<size_t>(chunk) * rows + row) * C + c] = sm[rr * (C + 1) + c];
+        }
+        __syncthreads();
+    }
+}
+
+// chunked block -> column-major scores [b][rows] with scatter through perm and
+// the clamp at zero (solver.py:181-184, 223-225).
+template <int C>
+__global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                      int64_t rows, int b, int nchunks,
+                                      const int64_t* __restrict__ perm, int clamp) {
+    constexpr int TR = 64;
+    __shared__ double sm[TR * (C + 1)];
+    const int64_t ntiles = (rows + TR - 1) / TR;
+    for (int64_t t = blockIdx.x; t < ntiles * nchunks; t += gridDim.x) {
+        const int chunk = static_cast<int>(t / ntiles);
+        const int64_t r0 = (t - static_cast<int64_t>(chunk) * ntiles) * TR;
+        for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
+            const int rr = e / C, c = e % C;
+            const int64_t row = r0 + rr;
+            sm[rr * (C + 1) + c] = row < rows ? src[(static_cast<size_t>(chunk) * rows + row) * C + c] : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
+            const int c = e / TR, rr = e % TR;
+            const int col = chunk * C + c;
+            const int64_t row = r0 + rr;
+            if (col < b && row < rows) {
+                double v = sm[rr * (C + 1) + c];
+                if (clamp) v = v > 0.0 ? v : 0.0;
+                const int64_t dstrow = perm ? perm[row] : row;
+                dst[static_cast<size_t>(col) * rows + dstrow] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int C>
+__global__ void broadcast_kernel(double* __restrict__ dst, const double* __restrict__ v,
+                                 int64_t rows, int b, int nchunks) {
+    const size_t total = static_cast<size_t>(nchunks) * rows * C;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(e % C);
+        const size_t rowc = e / C;
+        const int chunk = static_cast<int>(rowc / rows);
+        const int64_t row = static_cast<int64_t>(rowc - static_cast<size_t>(chunk) * rows);
+        dst[e] = (chunk * C + c < b) ? v[row] : 0.0;
+    }
+}
+
+// CTAs per chunk for the streaming kernels
+inline int stream_ctas_per_chunk(int64_t rows, int C, int nchunks) {
+    const int vec = C >= 2 ? 2 : 1;
+    const int64_t pairs = rows * C / vec;
+    int64_t nb = (pairs + kThreads * 4 - 1) / (kThreads * 4);
+    const int64_t cap = std::max<int64_t>(1, (2 * kMaxCtasPerChunk + nchunks - 1) / nchunks);
+    nb = std::max<int64_t>(1, std::min<int64_t>(nb, cap));
+    return static_cast<int>(nb);
+}
+
+#define KZ_DISPATCH_C(C, ...)                                 \
+    switch (C) {                                              \
+        case 1: { constexpr int CC = 1; __VA_ARGS__; } break;  \
+        case 2: { constexpr int CC = 2; __VA_ARGS__; } break;  \
+        case 4: { constexpr int CC = 4; __VA_ARGS__; } break;  \
+        case 8: { constexpr int CC = 8; __VA_ARGS__; } break;  \
+        case 16: { constexpr int CC = 16; __VA_ARGS__; } break; \
+        case 32: { constexpr int CC = 32; __VA_ARGS__; } break; \
+        default: return fail(KZ_EARG, "unsupported chunk width"); \
+    }
+
+}  // namespace kz

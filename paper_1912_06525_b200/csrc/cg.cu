@@ -1,0 +1,262 @@
+// cg.cu -- K2: batched textbook CG for Katz queries (query_cg_baseline / cg).
+//
+// One call solves b query columns of (I - beta*A) x = beta*A e_q.  Each
+// column runs the recurrence of cg() (solver.py:62-101) exactly -- the same
+// scalar formulas, the same stop test ||r|| <= tol*||b||, the same
+// non-positive-curvature error -- and is frozen (masked) once it stops, so
+// its iteration count is its own.  Per iteration three kernels run:
+//   spmm   q = p - beta*A p, column dots p.q, step length a = rs/pq
+//   update r -= a*q, column dots r.r, stop test, beta_cg = rs_new/rs
+//   pupd   x += a*p (deferred from solver.py:87), p = r + beta_cg*p
+// Moving `x += a*p` into the p-update pass keeps every rounding identical to
+// the reference order while saving one read+write of p and x per iteration.
+// The host only polls a device counter of active columns, one iteration
+// behind the GPU, so the device queue never drains.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "driver.cuh"
+
+using namespace kz;
+
+namespace {
+
+struct CgWork {
+    int C, nchunks, bpad, nb;
+    double *x, *r, *p, *q;
+    SpmmScratch sp;
+    RedScratch red;
+    SolveState st;
+    int64_t* qpos;
+};
+
+void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w) {
+    w.C = default_chunk(b);
+    w.nchunks = (b + w.C - 1) / w.C;
+    w.bpad = w.nchunks * w.C;
+    w.nb = stream_ctas_per_chunk(g->rows, w.C, w.nchunks);
+    const size_t blk = static_cast<size_t>(w.bpad) * g->rows;
+    w.x = cv.take<double>(blk);
+    w.r = cv.take<double>(blk);
+    w.p = cv.take<double>(blk);
+    w.q = cv.take<double>(blk);
+    carve_spmm_scratch(cv, g, w.nchunks, w.C, w.sp);
+    w.red.nb = w.nb;
+    w.red.part = cv.take<double>(static_cast<size_t>(w.nchunks) * w.nb * w.C);
+    w.red.cnt = cv.take<int32_t>(w.nchunks);
+    SolveState& s = w.st;
+    // state block: everything zero-initialised by one memset (see kz_cg_batch)
+    s.rs = cv.take<double>(w.bpad);
+    s.alpha = cv.take<double>(w.bpad);
+    s.betac = cv.take<double>(w.bpad);
+    s.thresh = cv.take<double>(w.bpad);
+    s.rnorm = cv.take<double>(w.bpad);
+    s.bnorm2 = cv.take<double>(w.bpad);
+    s.rr = cv.take<double>(w.bpad);
+    s.iters = cv.take<int64_t>(w.bpad);
+    s.active = cv.take<int32_t>(w.bpad);
+    s.xstamp = cv.take<int32_t>(w.bpad);
+    s.status = cv.take<int32_t>(w.bpad);
+    s.converged = cv.take<int32_t>(w.bpad);
+    s.chunk_active = cv.take<int32_t>(w.nchunks);
+    s.chunk_xstamp = cv.take<int32_t>(w.nchunks);
+    s.n_active = cv.take<int32_t>(1);
+    s.err = cv.take<int32_t>(1);
+    w.qpos = cv.take<int64_t>(w.bpad);
+}
+
+
+}  // namespace
+
+extern "C" size_t kz_cg_workspace_bytes(const kz_graph* g, int32_t b) {
+    if (!g || b < 1) return 0;
+    Carver cv(nullptr, 0);
+    CgWork w;
+    carve_cg(cv, g, b, w);
+    return cv.off + 256;
+}
+
+
+extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, size_t ws_bytes,
+                           void* stream) {
+    clear_error();
+    if (!g || !a) return fail(KZ_EARG, "NULL argument");
+    if (g->rows != g->cols) return fail(KZ_EARG, "CG needs a square operator");
+    if (a->b < 1) return fail(KZ_EARG, "empty batch");
+    if (!a->scores || !a->reports) return fail(KZ_EARG, "NULL outputs");
+    if (!a->rhs && !a->qpos) return fail(KZ_EARG, "need qpos or rhs");
+    if (!ws || ws_bytes < kz_cg_workspace_bytes(g, a->b)) return fail(KZ_EARG, "workspace too small");
+    const int b = a->b;
+    const int64_t n = g->rows;
+    if (a->qpos && !a->rhs)
+        for (int j = 0; j < b; ++j)
+            if (a->qpos[j] < 0 || a->qpos[j] >= n) return fail(KZ_EARG, "query position out of range");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    Carver cv(ws, ws_bytes);
+    CgWork w;
+    carve_cg(cv, g, b, w);
+    SolveState& s = w.st;
+    s.b = b;
+    s.bpad = w.bpad;
+    s.C = w.C;
+    s.nchunks = w.nchunks;
+    s.rows = n;
+    s.tol = a->tol;
+    s.max_iter = a->max_iter > 0 ? a->max_iter : 10 * n;
+    const int C = w.C, nchunks = w.nchunks, nb = w.nb;
+
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (a->device_ms) {
+        KZ_CUDA(cudaEventCreate(&e0));
+        KZ_CUDA(cudaEventCreate(&e1));
+        KZ_CUDA(cudaEventRecord(e0, st));
+    }
+    // zero state + counters (contiguous from s.rs to the end of qpos)
+    KZ_CUDA(cudaMemsetAsync(s.rs, 0, reinterpret_cast<char*>(w.qpos) - reinterpret_cast<char*>(s.rs), st));
+    KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nchunks, st));
+    if (int rc = zero_spmm_counters(g, nchunks, w.sp, st)) return rc;
+    const size_t blk_bytes = sizeof(double) * static_cast<size_t>(w.bpad) * n;
+    KZ_CUDA(cudaMemsetAsync(w.x, 0, blk_bytes, st));
+
+    const unsigned sgrid = static_cast<unsigned>(nchunks) * nb;
+    const unsigned tgrid = static_cast<unsigned>(std::min<int64_t>(
+        static_cast<int64_t>(kMaxCtasPerChunk) * 2, ((n + 63) / 64) * nchunks));
+
+    // right-hand side
+    if (a->rhs) {
+        KZ_DISPATCH_C(C, load_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.r, a->rhs, n, b, nchunks); ::kz::note_launch());
+    } else {
+        KZ_CUDA(cudaMemsetAsync(w.r, 0, blk_bytes, st));
+        KZ_CUDA(cudaMemcpyAsync(w.qpos, a->qpos, sizeof(int64_t) * b, cudaMemcpyHostToDevice, st));
+        KZ_DISPATCH_C(C, scatter_rhs_kernel<CC><<<b, kThreads, 0, st>>>(w.r, n, g->rowptr, g->colidx, w.qpos, b, a->beta); ::kz::note_launch());
+    }
+    KZ_LAUNCH_CHECK();
+    // ||b||, optional start vector (solver.py:51-59), init finalize
+    KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, w.red,
+                                                                     a->x0 ? FIN_INIT_B : FIN_INIT_BR,
+                                                                     s, nullptr, 0); ::kz::note_launch());
+    KZ_LAUNCH_CHECK();
+    if (a->x0) {
+        KZ_DISPATCH_C(C, broadcast_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.x, a->x0, n, b, nchunks); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+        SpmmArgs sa = make_spmm_args(g, w.sp);
+        sa.Xg = w.x;
+        sa.Xs = w.x;
+        sa.Z = w.r;
+        sa.Y = w.r;
+        sa.s0 = 1.0;
+        sa.s1 = -1.0;
+        sa.s2 = a->beta;  // r = b - (x - beta*A x)
+        sa.want_dot = 0;
+        if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
+        KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+    }
+    KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));
+
+    const double work = static_cast<double>(g->nnz + n) * w.bpad;
+    const int lag = work > 2e7 ? 1 : 3;
+    auto launch_iter = [&](int k) -> int {
+        SpmmArgs sa = make_spmm_args(g, w.sp);
+        sa.Xg = w.p;
+        sa.Xs = w.p;
+        sa.Z = nullptr;
+        sa.Y = w.q;
+        sa.s0 = 0.0;
+        sa.s1 = 1.0;
+        sa.s2 = -a->beta;
+        sa.D = nullptr;
+        sa.chunk_active = s.chunk_active;
+        sa.want_dot = 1;
+        sa.hook.mode = 1;
+        sa.hook.b = b;
+        sa.hook.rs = s.rs;
+        sa.hook.alpha = s.alpha;
+        sa.hook.active = s.active;
+        sa.hook.xstamp = s.xstamp;
+        sa.hook.chunk_xstamp = s.chunk_xstamp;
+        sa.hook.status = s.status;
+        sa.hook.err = s.err;
+        sa.hook.n_active = s.n_active;
+        sa.hook.iter = k;
+        if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
+        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, w.red, FIN_CG_CONV, s, k); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, w.r, n, nb, s, k); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+        return KZ_OK;
+    };
+    int64_t ran = 0;
+    int rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
+    if (rc) return rc;
+
+    KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, b, nchunks, a->perm, a->clamp); ::kz::note_launch());
+    KZ_LAUNCH_CHECK();
+    if (a->device_ms) {
+        KZ_CUDA(cudaEventRecord(e1, st));
+    }
+    // reports
+    std::vector<int64_t> iters(b);
+    std::vector<int32_t> conv(b), status(b);
+    std::vector<double> rnorm(b), bnorm2(b);
+    KZ_CUDA(cudaMemcpyAsync(iters.data(), s.iters, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaMemcpyAsync(conv.data(), s.converged, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaMemcpyAsync(status.data(), s.status, sizeof(int32_t) * b, cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaMemcpyAsync(rnorm.data(), s.rnorm, sizeof(double) * b, cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaMemcpyAsync(bnorm2.data(), s.bnorm2, sizeof(double) * b, cudaMemcpyDeviceToHost, st));
+    KZ_CUDA(cudaStreamSynchronize(st));
+    if (a->device_ms) {
+        KZ_CUDA(cudaEventElapsedTime(a->device_ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    bool notspd = false;
+    for (int j = 0; j < b; ++j) {
+        a->reports[j].iterations = iters[j];
+        a->reports[j].converged = conv[j];
+        a->reports[j].status = status[j];
+        a->reports[j].final_residual_norm = rnorm[j];
+        a->reports[j].rhs_norm = std::sqrt(bnorm2[j]);
+        notspd = notspd || status[j] == KZ_ENOTSPD;
+    }
+    if (notspd) return fail(KZ_ENOTSPD, "operator is not positive definite");
+    return KZ_OK;
+}
+
+extern "C" int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out,
+                         void* stream) {
+    clear_error();
+    if (n < 1 || b < 1 || !X || !Y || !out) return fail(KZ_EARG, "bad coldot arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // column-major == chunk width 1, one chunk per column
+    const int nb = stream_ctas_per_chunk(n, 1, b);
+    RedScratch red;
+    red.nb = nb;
+    static thread_local double* part = nullptr;
+    static thread_local int32_t* cnt = nullptr;
+    static thread_local size_t cap = 0, capb = 0;
+    const size_t need = static_cast<size_t>(b) * nb;
+    if (need > cap) {
+        if (part) cudaFree(part);
+        part = nullptr;
+        cap = 0;
+        KZ_CUDA(cudaMalloc(&part, sizeof(double) * need));
+        cap = need;
+    }
+    if (static_cast<size_t>(b) > capb) {
+        if (cnt) cudaFree(cnt);
+        cnt = nullptr;
+        capb = 0;
+        KZ_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * b));
+        capb = b;
+    }
+    red.part = part;
+    red.cnt = cnt;
+    KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * b, st));
+    SolveState s;
+    coldot_kernel<1><<<static_cast<unsigned>(b) * nb, kThreads, 0, st>>>(X, Y, n, red, FIN_WRITE, s, out, 0); ::kz::note_launch();
+    KZ_LAUNCH_CHECK();
+    return KZ_OK;
+}

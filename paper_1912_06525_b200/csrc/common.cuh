@@ -1,0 +1,68 @@
+// common.cuh -- shared helpers for libkatzb200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "katzb200.h"
+
+namespace kz {
+
+int fail(int code, const std::string& msg);  // records msg, returns code
+void clear_error();
+void note_launch();  // counts every kernel launch of the library (kz_launch_count)
+
+#define KZ_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return ::kz::fail(e_ == cudaErrorMemoryAllocation ? KZ_EOOM : KZ_ECUDA,     \
+                              std::string(#call) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+#define KZ_LAUNCH_CHECK()                                                               \
+    do {                                                                                \
+        cudaError_t e_ = cudaGetLastError();                                            \
+        if (e_ != cudaSuccess)                                                          \
+            return ::kz::fail(KZ_ECUDA, std::string("kernel launch: ") +                \
+                                            cudaGetErrorString(e_));                    \
+    } while (0)
+
+constexpr int kThreads = 256;        // threads per CTA for the streaming kernels
+constexpr int kWarps = kThreads / 32;
+constexpr int kNumSMs = 148;         // B200
+constexpr int kMaxCtasPerChunk = kNumSMs * 8;
+
+// Bump allocator over a caller-provided workspace (256-byte aligned slices).
+struct Carver {
+    char* base;
+    size_t off = 0;
+    size_t cap;
+    Carver(void* b, size_t c) : base(static_cast<char*>(b)), cap(c) {}
+    template <class T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += count * sizeof(T);
+        return p;
+    }
+    bool ok() const { return off <= cap; }
+};
+
+// Layout helper: the chunked node-major block [b/C][rows][C].
+__host__ __device__ inline size_t blk_index(int64_t rows, int C, int64_t i, int j) {
+    return (static_cast<size_t>(j / C) * rows + i) * C + (j % C);
+}
+
+// Supported chunk widths (columns per chunk) and the default choice for b.
+inline bool chunk_ok(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32; }
+inline int default_chunk(int b) {
+    if (b >= 16) return 16;
+    int c = 1;
+    while (c < b) c <<= 1;
+    return c;
+}
+
+}  // namespace kz

@@ -1,0 +1,287 @@
+"""Graphs in CSR form, the reference's graph rules, and the device operator.
+
+Host-side ingestion mirrors lrckatz.graph (graph.py:39-326): the same CSR
+invariants (symmetric, sorted columns, no self loops or duplicates,
+``original_ids`` strictly increasing), the same largest-component rule and
+the same spectral-norm estimator.  Ingestion is not the hot path; it only
+produces the operator that ``DeviceOperator`` uploads once (int32 column
+indices, no stored values) for the sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+class GraphParseError(ValueError):
+    """Malformed edge-list input (graph.py:17-24)."""
+
+
+class ConvergenceError(RuntimeError):
+    """Iteration budget exhausted; ``estimate`` holds the last value (graph.py:27-32)."""
+
+    def __init__(self, message, estimate):
+        super().__init__(message)
+        self.estimate = estimate
+
+
+class InadmissibleAlphaError(ValueError):
+    """Damping factor outside (0, 1/spectral_norm) (graph.py:35-36)."""
+
+
+@dataclass(frozen=True, eq=False)
+class Graph:
+    """Undirected graph in CSR form (graph.py:39-108)."""
+
+    n: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    original_ids: np.ndarray
+
+    @property
+    def num_edges(self):
+        return self.col_indices.size // 2
+
+    @property
+    def nnz(self):
+        return int(self.col_indices.size)
+
+    def degree(self, u):
+        return int(self.row_offsets[u + 1] - self.row_offsets[u])
+
+    def degrees(self):
+        return np.diff(self.row_offsets)
+
+    def neighbors(self, u):
+        return self.col_indices[self.row_offsets[u] : self.row_offsets[u + 1]]
+
+    def internal_id(self, original):
+        pos = int(np.searchsorted(self.original_ids, original))
+        if pos == self.n or self.original_ids[pos] != original:
+            raise KeyError(f"unknown node id {original}")
+        return pos
+
+    def adjacency(self):
+        import scipy.sparse as sp
+
+        return sp.csr_matrix(
+            (np.ones(self.col_indices.size), self.col_indices, self.row_offsets),
+            shape=(self.n, self.n),
+        )
+
+
+def csr_from_pairs(u, v, n):
+    """Symmetric, deduplicated, loop-free CSR from endpoint arrays.
+
+    Same result as from_edges (graph.py:111-148): columns sorted within each
+    row.  Vectorised: one sort of the directed keys src*n+dst.
+    """
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    lo = np.minimum(u, v)
+    hi = np.maximum(u, v)
+    und = np.unique(lo * n + hi)
+    lo, hi = und // n, und % n
+    del und
+    keys = np.concatenate([lo * n + hi, hi * n + lo])
+    del lo, hi
+    keys.sort(kind="stable")
+    src = keys // n
+    dst = keys % n
+    del keys
+    counts = np.bincount(src, minlength=n)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    return offsets, dst
+
+
+def from_edges(edges, n=None, original_ids=None):
+    """Build a Graph from (u, v) internal-id pairs (graph.py:111-148)."""
+    arr = np.asarray(edges if isinstance(edges, np.ndarray) else list(edges), dtype=np.int64)
+    if arr.size == 0:
+        arr = arr.reshape(0, 2)
+    if arr.ndim != 2 or arr.shape[1] != 2:
+        raise ValueError("edges must be (m, 2)")
+    if n is None:
+        if arr.size == 0:
+            raise ValueError("cannot infer node count from empty edge set")
+        n = int(arr.max()) + 1
+    if arr.size and (arr.min() < 0 or arr.max() >= n):
+        raise ValueError("edge endpoint out of range")
+    offsets, dst = csr_from_pairs(arr[:, 0], arr[:, 1], n)
+    if original_ids is None:
+        original_ids = np.arange(n, dtype=np.int64)
+    else:
+        original_ids = np.asarray(original_ids, dtype=np.int64)
+        if original_ids.shape != (n,):
+            raise ValueError("original_ids has wrong length")
+    return Graph(n=n, row_offsets=offsets, col_indices=dst, original_ids=original_ids)
+
+
+def largest_connected_component(g):
+    """Largest component, ties to the one holding the smallest original id
+    (graph.py:232-261); internal ids relabelled in increasing order."""
+    if g.n == 0:
+        raise ValueError("empty graph")
+    import scipy.sparse.csgraph as csgraph
+
+    count, labels = csgraph.connected_components(g.adjacency(), directed=False)
+    if count == 1:
+        return g
+    sizes = np.bincount(labels, minlength=count)
+    # the reference numbers components by their smallest node; pick, among the
+    # largest ones, the component whose smallest node is smallest
+    first = np.full(count, g.n, dtype=np.int64)
+    np.minimum.at(first, labels, np.arange(g.n))
+    cands = np.flatnonzero(sizes == sizes.max())
+    best = cands[np.argmin(first[cands])]
+    keep = np.flatnonzero(labels == best)
+    remap = np.full(g.n, -1, dtype=np.int64)
+    remap[keep] = np.arange(keep.size)
+    deg = np.diff(g.row_offsets)[keep]
+    offsets = np.zeros(keep.size + 1, dtype=np.int64)
+    np.cumsum(deg, out=offsets[1:])
+    # a component is closed under adjacency, so its rows keep every column
+    row_of = np.repeat(np.arange(g.n), np.diff(g.row_offsets))
+    mask = labels[row_of] == best
+    cols = remap[g.col_indices[mask]]
+    return Graph(n=int(keep.size), row_offsets=offsets, col_indices=cols,
+                 original_ids=g.original_ids[keep].copy())
+
+
+def hardest_alpha(norm):
+    """1/(norm + 1) (graph.py:300-308)."""
+    if norm < 0:
+        raise ValueError("spectral norm must be nonnegative")
+    return 1.0 / (norm + 1.0)
+
+
+@dataclass(frozen=True)
+class KatzParams:
+    """Validated (alpha, spectral_norm) pair (graph.py:311-326)."""
+
+    alpha: float
+    spectral_norm: float
+
+    def __post_init__(self):
+        if not (self.alpha > 0.0) or not (self.alpha * self.spectral_norm < 1.0):
+            raise InadmissibleAlphaError(
+                f"alpha={self.alpha} outside (0, 1/{self.spectral_norm})"
+            )
+
+
+class DeviceOperator:
+    """A binary CSR pattern resident on the GPU (kz_graph handle).
+
+    rows x cols pattern; rowptr int64[rows+1], colidx int32[nnz] (numpy or
+    torch CUDA tensors).  Immutable; freed with the object.
+    """
+
+    def __init__(self, rowptr, colidx, rows, cols=None):
+        lib = _lib.load()
+        self._lib = lib
+        self.rows = int(rows)
+        self.cols = int(rows if cols is None else cols)
+        keep = []
+        if isinstance(rowptr, np.ndarray):
+            rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+            keep.append(rp)
+            rp_ptr = ctypes.c_void_p(rp.ctypes.data)
+            nnz = int(rp[-1])
+        else:
+            rp = rowptr.contiguous()
+            keep.append(rp)
+            rp_ptr = ctypes.c_void_p(rp.data_ptr())
+            nnz = int(rp[-1].item())
+        if isinstance(colidx, np.ndarray):
+            ci = np.ascontiguousarray(colidx, dtype=np.int32)
+            keep.append(ci)
+            ci_ptr = ctypes.c_void_p(ci.ctypes.data)
+        else:
+            ci = colidx.contiguous()
+            keep.append(ci)
+            ci_ptr = ctypes.c_void_p(ci.data_ptr())
+        _lib.torch_cuda()  # a device must exist
+        h = ctypes.c_void_p()
+        _lib.check(lib.kz_graph_create(self.rows, self.cols, nnz, rp_ptr, ci_ptr, ctypes.byref(h)))
+        self.handle = h
+        self.nnz = nnz
+        vals = [ctypes.c_int64() for _ in range(5)]
+        _lib.check(lib.kz_graph_info(h, *[ctypes.byref(v) for v in vals]))
+        self.nlong = vals[3].value
+        self.nitems = vals[4].value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.kz_graph_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def spmm(self, Xg, Y, *, b, chunk=1, Xs=None, Z=None, s0=0.0, s1=0.0, s2=1.0, D=None, dots=None):
+        """Y = s0*Z + s1*Xs + s2*(A Xg) on device blocks (layout [b/C][.][C])."""
+        torch = _lib.torch_cuda()
+        nbytes = self._lib.kz_spmm_workspace_bytes(self.handle, b, chunk)
+        ws = _lib.Workspace.get(torch, nbytes, slot="spmm")
+        _lib.check(
+            self._lib.kz_spmm(
+                self.handle, b, chunk, _lib.ptr(Xg), _lib.ptr(Xs), _lib.ptr(Z), _lib.ptr(Y),
+                float(s0), float(s1), float(s2), _lib.ptr(D), _lib.ptr(dots),
+                _lib.ptr(ws), ws.numel(), _lib.stream_ptr(torch),
+            )
+        )
+        return Y
+
+
+def device_operator(g):
+    """Upload a Graph's adjacency pattern (natural order)."""
+    return DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32, copy=False), g.n)
+
+
+def spectral_norm(g, tol=1e-7, max_iter=10000, op=None):
+    """Largest |eigenvalue| of A by power iteration on A@A (graph.py:264-297),
+    with both products run by the K1 SpMM on the device."""
+    if g.n == 0:
+        raise ValueError("empty graph")
+    if g.col_indices.size == 0:
+        return 0.0
+    torch = _lib.torch_cuda()
+    lib = _lib.load()
+    op = op or device_operator(g)
+    n = g.n
+    v = torch.full((n,), 1.0 / np.sqrt(n), dtype=torch.float64, device="cuda")
+    t = torch.empty_like(v)
+    w = torch.empty_like(v)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    st = _lib.stream_ptr(torch)
+
+    def dot(x, y):
+        _lib.check(lib.kz_coldot(n, 1, _lib.ptr(x), _lib.ptr(y), _lib.ptr(out), st))
+        return float(out.item())
+
+    last = 0.0
+    for _ in range(max_iter):
+        op.spmm(v, t, b=1)
+        op.spmm(t, w, b=1)
+        est = np.sqrt(dot(v, w))
+        nw = np.sqrt(dot(w, w))
+        if nw == 0.0:
+            return 0.0
+        v = w / nw
+        w = torch.empty_like(v)
+        if abs(est - last) <= tol * max(est, 1e-300):
+            op.spmm(v, t, b=1)
+            return float(np.sqrt(dot(t, t)))
+        last = est
+    raise ConvergenceError(
+        f"spectral norm estimate did not settle in {max_iter} iterations", float(last)
+    )

@@ -1,0 +1,184 @@
+"""Link-prediction scoring on the GPU with the reference's API.
+
+Mirrors the scoring half of lrckatz.linkpred (linkpred.py:115-207):
+``pearson``, ``katz_rank`` (masked top-s by exact Katz score) and
+``sparse_katz`` (the anchor-profile Pearson rerank), plus batched variants
+that run every query of a batch through one solve, one masked top-k
+(K4) and, for sparse_katz, deduplicated anchor solves and the K7 rerank.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from . import solver
+
+
+@dataclass(eq=False)
+class RankedPrediction:
+    """Ranked candidates (original id, score) for one query (linkpred.py:27-38)."""
+
+    query: int
+    candidates: list
+    method: str
+
+
+def pearson(x, y):
+    """Pearson correlation; 0.0 for a constant vector, clipped to [-1, 1]
+    (linkpred.py:115-133).  Scalar utility: evaluated on the host."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if x.ndim != 1 or x.shape != y.shape:
+        raise ValueError("inputs must be equal-length vectors")
+    if x.size < 2:
+        raise ValueError("need at least two samples")
+    xc = x - x.mean()
+    yc = y - y.mean()
+    sx = np.linalg.norm(xc)
+    sy = np.linalg.norm(yc)
+    if sx == 0.0 or sy == 0.0:
+        return 0.0
+    return float(np.clip((xc @ yc) / (sx * sy), -1.0, 1.0))
+
+
+def topk_device(scores, k, mask_op=None, mask_rows=None, self_ids=None):
+    """K4 masked top-k over the columns of scores (cuda fp64 [b][n]).
+
+    Returns (ids int64 [b][k], vals fp64 [b][k], counts int32 [b]) on the
+    device; ids are positions in the scores' order (internal ids)."""
+    torch = _lib.torch_cuda()
+    lib = _lib.load()
+    b, n = scores.shape
+    k = int(k)
+    ids = torch.empty((b, k), dtype=torch.int64, device="cuda")
+    vals = torch.empty((b, k), dtype=torch.float64, device="cuda")
+    counts = torch.empty((b,), dtype=torch.int32, device="cuda")
+    args = _lib.KzTopkArgs()
+    args.b = b
+    args.k = k
+    args.n = n
+    args.scores = scores.data_ptr()
+    keep = []
+    if mask_op is not None and mask_rows is not None:
+        args.mask_graph = mask_op.handle.value
+        arr, p = _lib.i64_array(mask_rows)
+        keep.append(arr)
+        args.mask_rows = p
+    if self_ids is not None:
+        arr, p = _lib.i64_array(self_ids)
+        keep.append(arr)
+        args.self_ids = p
+    args.ids_out = ids.data_ptr()
+    args.vals_out = vals.data_ptr()
+    args.count_out = counts.data_ptr()
+    ws = _lib.Workspace.get(torch, lib.kz_topk_workspace_bytes(b, n, k), slot="topk")
+    _lib.check(lib.kz_topk_batch(ctypes.byref(args), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(torch)))
+    return ids, vals, counts
+
+
+def _query_batch_state(idx, qs, tol):
+    scores, _ = solver.query_batch(idx, qs, tol=tol, device=True)
+    internal = idx.internal_ids(qs)
+    return scores, internal
+
+
+def katz_rank_batch(idx, qs, s, tol=1e-10):
+    """katz_rank for many queries: one batched solve + one masked top-s."""
+    if s < 1:
+        raise ValueError("s must be >= 1")
+    qs = np.atleast_1d(np.asarray(qs, dtype=np.int64))
+    try:
+        scores, internal = _query_batch_state(idx, qs, tol)
+    except KeyError as err:
+        raise solver.UnknownNodeError(str(err)) from None
+    s_eff = min(int(s), idx.n)
+    ids, vals, counts = topk_device(scores, s_eff, idx.mask_operator(), internal, internal)
+    ids, vals, counts = ids.cpu().numpy(), vals.cpu().numpy(), counts.cpu().numpy()
+    out = []
+    for j, q in enumerate(qs):
+        m = int(counts[j])
+        cands = [(int(idx.id_map[ids[j, c]]), float(vals[j, c])) for c in range(m)]
+        out.append(RankedPrediction(query=int(q), candidates=cands, method="katz"))
+    return out
+
+
+def katz_rank(idx, q, s, tol=1e-10):
+    """Top-s predicted links for q by exact Katz score (linkpred.py:155-162)."""
+    if s < 1:
+        raise ValueError("s must be >= 1")
+    return katz_rank_batch(idx, [q], s, tol)[0]
+
+
+def sparse_katz_batch(idx, qs, s, T=None, tol=1e-10, anchor_batch=256):
+    """sparse_katz for many queries (linkpred.py:165-207), batched.
+
+    The anchor solves of all queries are deduplicated and run in batches of
+    ``anchor_batch`` columns; each batch's scores are gathered straight into
+    the candidates' profiles (K7 gather) and dropped, so the device holds at
+    most one batch of anchor score vectors."""
+    if s < 1:
+        raise ValueError("s must be >= 1")
+    if T is None:
+        T = s + 1
+    if T < 1:
+        raise ValueError("need at least one anchor")
+    if T > idx.n - 1:
+        raise ValueError(f"T={T} anchors not available on {idx.n} nodes")
+    torch = _lib.torch_cuda()
+    lib = _lib.load()
+    st = _lib.stream_ptr(torch)
+    qs = np.atleast_1d(np.asarray(qs, dtype=np.int64))
+    try:
+        scores, internal = _query_batch_state(idx, qs, tol)
+    except KeyError as err:
+        raise solver.UnknownNodeError(str(err)) from None
+    b, n = scores.shape
+    s_eff = min(int(s), n)
+    top, top_vals, counts = topk_device(scores, s_eff, idx.mask_operator(), internal, internal)
+    anc, _, anc_counts = topk_device(scores, T, None, None, internal)
+    T1 = T + 1
+    # reference profile [K(q,q), K(a_i,q)]  (linkpred.py:189-191)
+    qidx = torch.as_tensor(internal, dtype=torch.int64, device="cuda")
+    rows = torch.arange(b, device="cuda")
+    ref = torch.empty((b, T1), dtype=torch.float64, device="cuda")
+    ref[:, 0] = scores[rows, qidx]
+    ref[:, 1:] = torch.gather(scores, 1, anc)
+    profiles = torch.empty((b, T1, s_eff), dtype=torch.float64, device="cuda")
+    profiles[:, 0, :] = top_vals
+    del scores
+    anc_host = anc.cpu().numpy()
+    uniq, inverse = np.unique(anc_host, return_inverse=True)
+    inverse = inverse.reshape(b, T)
+    for s0 in range(0, uniq.size, anchor_batch):
+        chunk = uniq[s0 : s0 + anchor_batch]
+        a_scores, _ = solver.query_batch(idx, idx.id_map[chunk], tol=tol, device=True)
+        sel = np.argwhere((inverse >= s0) & (inverse < s0 + chunk.size))
+        trip = np.stack([inverse[sel[:, 0], sel[:, 1]] - s0, sel[:, 0], sel[:, 1] + 1], axis=1)
+        trip_d = torch.as_tensor(np.ascontiguousarray(trip, dtype=np.int64), device="cuda")
+        _lib.check(lib.kz_profile_gather(_lib.ptr(a_scores), n, int(trip.shape[0]), _lib.ptr(trip_d),
+                                         _lib.ptr(top), _lib.ptr(counts), s_eff, _lib.ptr(profiles),
+                                         T1, st))
+        del a_scores
+    corr = torch.empty((b, s_eff), dtype=torch.float64, device="cuda")
+    order = torch.empty((b, s_eff), dtype=torch.int64, device="cuda")
+    _lib.check(lib.kz_pearson_rerank(_lib.ptr(profiles), _lib.ptr(ref), _lib.ptr(top), _lib.ptr(top_vals),
+                                     _lib.ptr(counts), b, T1, s_eff, _lib.ptr(corr), _lib.ptr(order), st))
+    top_h, corr_h, order_h, counts_h = (top.cpu().numpy(), corr.cpu().numpy(), order.cpu().numpy(),
+                                        counts.cpu().numpy())
+    out = []
+    for j, q in enumerate(qs):
+        m = int(counts_h[j])
+        cands = [(int(idx.id_map[top_h[j, order_h[j, c]]]), float(corr_h[j, order_h[j, c]]))
+                 for c in range(m)]
+        out.append(RankedPrediction(query=int(q), candidates=cands, method="sparse-katz"))
+    return out
+
+
+def sparse_katz(idx, q, s, T=None, tol=1e-10):
+    """Rerank the top-s Katz candidates by anchor-profile correlation
+    (linkpred.py:165-207)."""
+    return sparse_katz_batch(idx, [q], s, T, tol)[0]

@@ -1,0 +1,256 @@
+"""GPU parity of K1 (SpMM), K2 (batched CG) and K4 (top-k) against the oracle.
+
+Tolerances (BASELINE.json north_star): scores within relative L2 1e-10 per
+query column, CG iteration counts within +/-1 of the same-recurrence CPU
+oracle; top-k identical apart from ties within tolerance.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import katz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def kz(torch):
+    import paper_1912_06525_b200 as kz
+
+    return kz
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def chunglu_fixture():
+    rec = np.load(os.path.join(GOLDEN, "chunglu2000_cg.npz"))
+    n = rec["row_offsets"].size - 1
+    return rec, n
+
+
+def to_blk(X, C):
+    """[n][b] -> chunked [b/C][n][C]"""
+    n, b = X.shape
+    return np.ascontiguousarray(X.T.reshape(b // C, C, n).transpose(0, 2, 1))
+
+
+def from_blk(Y, n, b, C):
+    return Y.reshape(b // C, n, C).transpose(0, 2, 1).reshape(b, n).T
+
+
+@pytest.mark.parametrize("graph", ["chunglu2000", "rmat12"])
+@pytest.mark.parametrize("b,C", [(1, 1), (4, 4), (16, 16), (32, 16), (32, 32), (8, 2)])
+def test_spmm_matches_scipy(torch, kz, graph, b, C):
+    if graph == "chunglu2000":
+        rec, n = chunglu_fixture()
+        off, col = rec["row_offsets"], rec["col_indices"]
+    else:
+        from paper_1912_06525_b200.generators import rmat_graph
+
+        g = rmat_graph(12, seed=3)
+        n, off, col = g.n, g.row_offsets, g.col_indices
+    a = O.csr_matrix(off, col, n)
+    op = kz.DeviceOperator(off, col.astype(np.int32), n)
+    rng = np.random.default_rng(b * 100 + C)
+    X = rng.standard_normal((n, b))
+    beta = 0.013
+    Xd = torch.as_tensor(to_blk(X, C)).cuda()
+    Yd = torch.empty_like(Xd)
+    dots = torch.empty(b, dtype=torch.float64, device="cuda")
+    op.spmm(Xd, Yd, b=b, chunk=C, Xs=Xd, s1=1.0, s2=-beta, dots=dots)
+    Y = from_blk(Yd.cpu().numpy(), n, b, C)
+    want = X - beta * (a @ X)
+    long_rows = np.diff(off) > 512
+    # short rows sum in CSR order with the same roundings as scipy: bit-exact
+    assert np.array_equal(Y[~long_rows], want[~long_rows])
+    assert np.abs(Y - want).max() <= 1e-13 * np.abs(want).max()
+    want_dots = np.einsum("ij,ij->j", X, want)
+    assert np.allclose(dots.cpu().numpy(), want_dots, rtol=1e-12, atol=0)
+    # deterministic: a second launch is bit-identical
+    Y2 = torch.empty_like(Xd)
+    op.spmm(Xd, Y2, b=b, chunk=C, Xs=Xd, s1=1.0, s2=-beta)
+    assert torch.equal(Yd, Y2)
+
+
+def test_cg_batch_matches_reference_cg_golden(torch, kz):
+    rec, n = chunglu_fixture()
+    g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"],
+                 original_ids=np.arange(n))
+    idx = kz.GraphIndex(g, float(rec["beta"]))
+    scores, reps = kz.query_cg_baseline_batch(idx, rec["queries"], tol=1e-8)
+    for j in range(len(rec["queries"])):
+        assert abs(reps[j].iterations - rec["iters"][j]) <= 1
+        assert reps[j].converged
+        assert rel(scores[j], rec["scores"][j]) <= REL_TOL
+        assert reps[j].final_residual_norm == pytest.approx(rec["resid"][j], rel=1e-6)
+
+
+def test_spectral_norm_matches_reference(torch, kz):
+    rec, n = chunglu_fixture()
+    g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"],
+                 original_ids=np.arange(n))
+    lam = kz.spectral_norm(g)
+    assert lam == pytest.approx(float(rec["spectral_norm"]), rel=1e-9)
+
+
+NAMES = ["k2", "p4", "p5split", "star5", "triangle", "er40", "er60", "ba300", "ba1200"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("tol", [1e-8, 1e-10])
+def test_query_cg_baseline_on_klrc_matches_reference(torch, kz, name, tol):
+    idx = kz.load_index(os.path.join(GOLDEN, f"{name}.klrc"))
+    rec = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    key = f"cg_{tol:.0e}"
+    scores, reps = kz.query_cg_baseline_batch(idx, rec["queries"], tol=tol)
+    for j in range(len(rec["queries"])):
+        assert abs(reps[j].iterations - rec[f"{key}_iters"][j]) <= 1
+        assert rel(scores[j], rec[f"{key}_scores"][j]) <= REL_TOL
+        assert reps[j].converged == bool(rec[f"{key}_conv"][j])
+    # single-query drop-in path
+    kv, rep = kz.query_cg_baseline(idx, int(rec["queries"][0]), tol=tol)
+    assert kv.scores.shape == (idx.n,) and kv.query == int(rec["queries"][0]) and kv.alpha == idx.alpha
+    assert rel(kv.scores, rec[f"{key}_scores"][0]) <= REL_TOL
+
+
+@pytest.mark.parametrize("name", ["er40", "ba300", "ba1200"])
+def test_cg_seeded_start_and_budget(torch, kz, name):
+    idx = kz.load_index(os.path.join(GOLDEN, f"{name}.klrc"))
+    rec = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    q0 = int(rec["queries"][0])
+    kv, rep = kz.query_cg_baseline(idx, q0, tol=1e-10, start_seed=5)
+    assert abs(rep.iterations - int(rec["cg_seed5_iters"])) <= 1
+    assert rel(kv.scores, rec["cg_seed5_scores"]) <= REL_TOL
+    kv, rep = kz.query_cg_baseline(idx, q0, tol=1e-12, max_iter=1)
+    assert rep.iterations == 1 and rep.converged == bool(rec["cg_budget1_conv"])
+    assert rel(kv.scores, rec["cg_budget1_scores"]) <= REL_TOL
+
+
+def test_unknown_node_and_not_spd(torch, kz):
+    idx = kz.load_index(os.path.join(GOLDEN, "er40.klrc"))
+    with pytest.raises(kz.UnknownNodeError):
+        kz.query_cg_baseline(idx, 10**9)
+    rec, n = chunglu_fixture()
+    g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"],
+                 original_ids=np.arange(n))
+    bad = kz.GraphIndex(g, 5.0 / float(rec["spectral_norm"]))  # I - 5A/lambda is indefinite
+    with pytest.raises(RuntimeError):
+        kz.query_cg_baseline_batch(bad, rec["queries"], tol=1e-12)
+
+
+def test_generic_cg_matches_direct_solve(torch, kz):
+    # tests/test_solver.py:32-58 on the device path
+    b = np.random.default_rng(0).standard_normal(30)
+    x, rep = kz.cg(lambda v: v, b)
+    assert rep.iterations == 1 and rep.converged and np.abs(x - b).max() < 1e-14
+    x, rep = kz.cg(lambda v: 2.0 * v, np.zeros(7))
+    assert rep.iterations == 0 and rep.converged and np.all(x == 0.0)
+    rng = np.random.default_rng(1)
+    q, _ = np.linalg.qr(rng.standard_normal((50, 50)))
+    a = (q * rng.uniform(0.5, 4.0, 50)) @ q.T
+    b = rng.standard_normal(50)
+    x, rep = kz.cg(lambda v: a @ v, b, tol=1e-10)
+    assert rep.converged and rel(x, np.linalg.solve(a, b)) < 1e-8
+    with pytest.raises(RuntimeError):
+        kz.cg(lambda v: -v, np.ones(4))
+
+
+def test_cg_katz_operator_single_call(torch, kz):
+    rec, n = chunglu_fixture()
+    op = kz.DeviceOperator(rec["row_offsets"], rec["col_indices"].astype(np.int32), n)
+    beta = float(rec["beta"])
+    q = int(rec["queries"][0])
+    rhs = np.zeros(n)
+    rhs[rec["col_indices"][rec["row_offsets"][q] : rec["row_offsets"][q + 1]]] = beta
+    x, rep = kz.cg(kz.KatzOperator(op, beta), rhs, tol=1e-8)
+    assert abs(rep.iterations - rec["iters"][0]) <= 1
+    assert rel(np.maximum(x, 0), rec["scores"][0]) <= REL_TOL
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "proxy16"])
+def test_cg_batch_at_config_sizes(torch, kz, cfg):
+    """cfg1 (Chung-Lu 10k, b=16) and the R-MAT-16 proxy (b=64) against the
+    CSR oracle on a sample of columns."""
+    from paper_1912_06525_b200.generators import CONFIGS, config_graph, sample_queries
+
+    g = config_graph(cfg)
+    lam = kz.spectral_norm(g)
+    beta = 0.5 / lam
+    idx = kz.GraphIndex(g, beta)
+    b = CONFIGS[cfg]["b"]
+    qs = sample_queries(g.original_ids, b, seed=0)
+    scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=1e-8, device=True)
+    a = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
+    for j in np.linspace(0, b - 1, 6).astype(int):
+        want, orep = O.query_cg_csr(a, beta, int(qs[j]), tol=1e-8)
+        assert abs(reps[j].iterations - orep.iterations) <= 1
+        assert rel(scores[j].cpu().numpy(), want) <= REL_TOL
+
+
+def test_topk_matches_lexsort(torch, kz):
+    rng = np.random.default_rng(4)
+    b, n = 7, 50_000
+    S = np.abs(rng.standard_normal((b, n)))
+    S[:, ::7] = np.round(S[:, ::7], 1)  # many exact ties
+    S[1, :] = 0.25  # all tied
+    S[2, : n // 2] = 0.0
+    Sd = torch.as_tensor(S).cuda()
+    self_ids = np.array([3, 10, 0, n - 1, 5, 6, 7])
+    for k in (1, 20, 100, 1000):
+        ids, vals, counts = kz.topk_device(Sd, k, None, None, self_ids)
+        ids, vals = ids.cpu().numpy(), vals.cpu().numpy()
+        for j in range(b):
+            cand = np.array([i for i in range(n) if i != self_ids[j]])
+            order = cand[np.lexsort((cand, -S[j][cand]))][:k]
+            assert list(ids[j]) == list(order)
+            assert np.array_equal(vals[j], S[j][order])
+
+
+def test_topk_masks_neighbours(torch, kz):
+    rec, n = chunglu_fixture()
+    op = kz.DeviceOperator(rec["row_offsets"], rec["col_indices"].astype(np.int32), n)
+    S = rec["scores"]
+    qs = rec["queries"]
+    Sd = torch.as_tensor(S).cuda()
+    for k in (5, 50, n):
+        ids, vals, counts = kz.topk_device(Sd, min(k, n), op, qs, qs)
+        ids, counts = ids.cpu().numpy(), counts.cpu().numpy()
+        for j, q in enumerate(qs):
+            nbrs = rec["col_indices"][rec["row_offsets"][q] : rec["row_offsets"][q + 1]]
+            want = O.candidate_order(n, S[j], int(q), nbrs, min(k, n))
+            assert counts[j] == len(want)
+            assert list(ids[j][: counts[j]]) == list(want)
+
+
+def test_katz_rank_graph_index_matches_oracle(torch, kz):
+    rec, n = chunglu_fixture()
+    g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"],
+                 original_ids=np.arange(n))
+    beta = float(rec["beta"])
+    idx = kz.GraphIndex(g, beta)
+    a = O.csr_matrix(rec["row_offsets"], rec["col_indices"], n)
+    solve = lambda i: O.query_cg_csr(a, beta, i, tol=1e-10)[0]  # noqa: E731
+    nbrs = lambda i: a.indices[a.indptr[i] : a.indptr[i + 1]]  # noqa: E731
+    preds = kz.katz_rank_batch(idx, rec["queries"][:4], 20)
+    for j, q in enumerate(rec["queries"][:4]):
+        want = O.katz_rank(solve, nbrs, np.arange(n), int(q), 20)
+        got = preds[j].candidates
+        assert [c for c, _ in got] == [c for c, _ in want]
+        assert np.allclose([v for _, v in got], [v for _, v in want], rtol=1e-9, atol=0)

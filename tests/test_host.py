@@ -1,0 +1,172 @@
+"""CPU tests of the host side: the C-ABI library, the KLRC reader, the
+index re-expression and the generators.  No kernel is launched here."""
+
+import ctypes
+import io
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+from oracle import katz_oracle as O
+
+import paper_1912_06525_b200 as kz
+from paper_1912_06525_b200 import _lib
+from paper_1912_06525_b200.index import (
+    IndexChecksumError,
+    IndexFormatError,
+    IndexMagicError,
+    IndexVersionError,
+    load_index,
+    save_index,
+)
+
+NAMES = ["k2", "p4", "p5split", "star5", "triangle", "er40", "er60", "ba300", "ba1200"]
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = _lib.header_symbols()
+    assert "kz_cg_batch" in syms and "kz_spmm" in syms and "kz_topk_batch" in syms
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.kz_version() == 1
+
+
+def test_library_is_sm100a():
+    so = os.path.join(ROOT, "paper_1912_06525_b200", "libkatzb200.so")
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_argument_errors_without_gpu():
+    lib = _lib.load()
+    # NULL handle / bad arguments are rejected before any device work
+    assert lib.kz_spmm(None, 1, 1, None, None, None, None, 0.0, 0.0, 0.0, None, None, None, 0, None) == _lib.KZ_EARG
+    assert b"NULL" in lib.kz_last_error()
+    h = ctypes.c_void_p()
+    rp = np.array([0, 1], dtype=np.int64)
+    assert lib.kz_graph_create(0, 0, 0, rp.ctypes.data, None, ctypes.byref(h)) == _lib.KZ_EARG
+    bad = np.array([0, 2, 1], dtype=np.int64)
+    assert lib.kz_graph_create(2, 2, 1, bad.ctypes.data, None, ctypes.byref(h)) == _lib.KZ_EARG
+    args = _lib.KzTopkArgs()
+    assert lib.kz_topk_batch(ctypes.byref(args), None, 0, None) == _lib.KZ_EARG
+    assert isinstance(_lib.error_from_status(_lib.KZ_EARG, lib), ValueError)
+    assert isinstance(_lib.error_from_status(_lib.KZ_ENOTSPD, lib), RuntimeError)
+    assert isinstance(_lib.error_from_status(_lib.KZ_ESPECTRUM, lib), kz.SpectrumError)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_klrc_reader_matches_oracle_and_roundtrips(name):
+    path = os.path.join(GOLDEN, f"{name}.klrc")
+    idx = load_index(path)
+    ix = O.read_klrc(path)
+    assert idx.n == ix.n and idx.n1 == ix.n1 and idx.n2 == ix.n2 and idx.lr.ell == ix.ell
+    assert idx.alpha == ix.alpha and idx.spectral_norm == ix.spectral_norm
+    assert np.array_equal(idx.bp.perm, ix.perm) and np.array_equal(idx.id_map, ix.id_map)
+    assert np.array_equal(idx.dc.factor, ix.L) and np.array_equal(idx.lr.vectors, ix.U)
+    sink = io.BytesIO()
+    save_index(idx, sink)
+    assert sink.getvalue() == open(path, "rb").read()  # bit-exact round trip
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_adjacency_recovered_from_factors(name):
+    idx = load_index(os.path.join(GOLDEN, f"{name}.klrc"))
+    rec = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    off, col = idx.adjacency_internal()
+    assert np.array_equal(off, rec["row_offsets"])
+    assert np.array_equal(col, rec["col_indices"])
+    # partition-order pattern is the permuted one
+    offp, colp = idx.adjacency_permuted()
+    n = idx.n
+    a = np.zeros((n, n))
+    a[np.repeat(np.arange(n), np.diff(off)), col] = 1
+    ap = a[np.ix_(idx.bp.perm, idx.bp.perm)]
+    r, c = np.nonzero(ap)
+    assert np.array_equal(colp, c) and np.array_equal(np.diff(offp), np.bincount(r, minlength=n))
+
+
+def test_rhs_for_position_is_exact_column():
+    idx = load_index(os.path.join(GOLDEN, "er40.klrc"))
+    ix = O.read_klrc(os.path.join(GOLDEN, "er40.klrc"))
+    for pos in (0, idx.n // 2, idx.n - 1):
+        got = idx.rhs_for_position(pos)
+        want = O.rhs_for_position(ix, pos)
+        assert np.abs(got - want).max() < 1e-15
+
+
+def _blob(name="er40"):
+    return open(os.path.join(GOLDEN, f"{name}.klrc"), "rb").read()
+
+
+def test_error_taxonomy():
+    blob = _blob()
+    with pytest.raises(IndexMagicError):
+        load_index(io.BytesIO(b"XLRC" + blob[4:]))
+    with pytest.raises(IndexChecksumError):
+        load_index(io.BytesIO(blob[:-1]))
+    with pytest.raises(IndexChecksumError):
+        load_index(io.BytesIO(blob[:10]))
+    import hashlib
+
+    payload = bytearray(blob[:-8])
+    payload[4:8] = struct.pack("<I", 2)
+    with pytest.raises(IndexVersionError):
+        load_index(io.BytesIO(bytes(payload) + hashlib.blake2b(bytes(payload), digest_size=8).digest()))
+    # structural damage behind a valid checksum (cf. tests/test_index.py:195-211)
+    payload = bytearray(blob[:-8])
+    payload[41:49] = struct.pack("<Q", 999)  # n1
+    with pytest.raises(IndexFormatError):
+        load_index(io.BytesIO(bytes(payload) + hashlib.blake2b(bytes(payload), digest_size=8).digest()))
+
+
+def test_every_byte_flip_is_detected():
+    blob = _blob("p5split")
+    for i in range(len(blob)):
+        bad = bytearray(blob)
+        bad[i] ^= 0x01
+        with pytest.raises(IndexFormatError):
+            load_index(io.BytesIO(bytes(bad)))
+
+
+def test_generators_reproduce_survey_sizes():
+    from paper_1912_06525_b200.generators import chung_lu_graph, rmat_graph, sample_queries
+
+    g = chung_lu_graph()
+    assert (g.n, g.nnz, int(g.degrees().max())) == (9924, 97754, 1208)
+    g = rmat_graph(16)
+    assert (g.n, g.nnz) == (46694, 1819054)
+    q = sample_queries(g.original_ids, 16, seed=0)
+    assert q.size == 16 and np.all(np.diff(q) > 0)
+    with pytest.raises(ValueError):
+        sample_queries(np.arange(3), 4)
+
+
+def test_from_edges_and_lcc_follow_reference_rules():
+    g = kz.from_edges([(0, 1), (1, 0), (1, 1), (2, 3), (4, 5), (5, 6)], n=8)
+    assert g.nnz == 8 and list(g.neighbors(1)) == [0]
+    lcc = kz.largest_connected_component(g)
+    # sizes {0,1}:2, {2,3}:2, {4,5,6}:3 -> the 3-node component
+    assert list(lcc.original_ids) == [4, 5, 6]
+    g2 = kz.from_edges([(0, 1), (2, 3)], n=4)
+    assert list(kz.largest_connected_component(g2).original_ids) == [0, 1]  # tie -> smallest id
+
+
+def test_pearson_host_closed_forms():
+    assert kz.pearson([1, 2, 3], [10, 20, 30]) == pytest.approx(1.0, abs=1e-12)
+    assert kz.pearson([1, 2, 3, 4, 5], [2, 1, 4, 3, 7]) == pytest.approx(0.824163383692134, abs=1e-12)
+    with pytest.raises(ValueError):
+        kz.pearson([1.0], [2.0])
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(ROOT, "paper_1912_06525_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in src.replace("oracle restatement", ""), fn
