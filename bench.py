@@ -124,6 +124,7 @@ def cpu_sample(g, beta, qs, tol, budget, threads):
     from oracle import katz_oracle as O
 
     a = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
+    qs = np.searchsorted(g.original_ids, np.asarray(qs))  # original -> internal ids
     done = 0
     iters = []
     t0 = time.perf_counter()

@@ -106,6 +106,70 @@ typedef struct kz_cg_args {
 size_t kz_cg_workspace_bytes(const kz_graph* g, int32_t b);
 int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, size_t ws_bytes, void* stream);
 
+/* Weighted operator (fp64 values), e.g. the block-diagonal M11^-1 whose
+ * dense per-part blocks replace BlockCholesky.solve (factor.py:89-106). */
+int kz_graph_create_weighted(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
+                             const int32_t* colidx, const double* vals, kz_graph** out);
+
+/* ---- LRC-Katz: batched Schur-complement PCG (query, solver.py:161-207) ----
+ * The handle borrows every operand (device memory owned by the caller):
+ * K1 operators of A in partition order (full n x n, A12 n1 x n2, A21 n2 x n1,
+ * A22 n2 x n2), the weighted block-diagonal M11^-1 (n1 x n1), the dense
+ * row-major L^-1 and (L^-1)^T (n2 x n2), U (n2 x ell) and (U diag(d))^T
+ * (ell x n2) with d = 1/(1-sigma) - 1 (factor.py:322-337).  sigma is read
+ * (host) only to raise KZ_ESPECTRUM when any sigma >= 1 (factor.py:329-330). */
+typedef struct kz_lrc kz_lrc;
+typedef struct kz_lrc_desc {
+    int64_t n, n1, n2, ell;
+    double beta;
+    const kz_graph* full;
+    const kz_graph* a12;
+    const kz_graph* a21;
+    const kz_graph* a22;
+    const kz_graph* minv;
+    const double* linv;
+    const double* linvT;
+    const double* u;
+    const double* udT;
+    const double* sigma; /* host double[ell] */
+} kz_lrc_desc;
+
+/* Query mode (f == NULL): column j solves query position qpos[j] (partition
+ * order) end to end -- rhs, Schur reduction, PCG with tol_eff, back
+ * substitution, whole-system residual, scatter through perm, clamp -- and
+ * writes scores out[j][n]; the report carries the inner PCG iterations and
+ * the true residual (solver.py:185-190).  PCG mode (f != NULL, device
+ * [b][n2]): lrc_pcg (solver.py:118-158) on the given Schur rhs, x into
+ * out[j][n2], recursive residual in the report. */
+typedef struct kz_lrc_args {
+    int32_t b;
+    int32_t chunk; /* 0: default */
+    int32_t clamp;
+    int32_t _pad;
+    const int64_t* qpos; /* host int64[b] */
+    const double* f;
+    double tol;
+    int64_t max_iter; /* <= 0: 10*n2 */
+    const double* x0; /* device double[n2] start vector (start_seed), or NULL */
+    const int64_t* perm;
+    double* out;
+    kz_report* reports;
+    float* device_ms;
+} kz_lrc_args;
+
+#define KZ_LRC_SCHUR 0     /* out = S in1                      (solver.py:113-115) */
+#define KZ_LRC_PRECOND 1   /* out = S~^-1 in1                  (factor.py:322-337) */
+#define KZ_LRC_SCHUR_RHS 2 /* out = in2 - M12' M11^-1 in1      (solver.py:104-110) */
+
+int kz_lrc_create(const kz_lrc_desc* d, kz_lrc** out);
+int kz_lrc_destroy(kz_lrc* h);
+int kz_lrc_info(const kz_lrc* h, int64_t* n, int64_t* n1, int64_t* n2, int64_t* ell);
+size_t kz_lrc_workspace_bytes(const kz_lrc* h, int32_t b, int32_t chunk);
+int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, size_t ws_bytes, void* stream);
+/* op in KZ_LRC_*; in1/in2/out column-major [b][rows] */
+int kz_lrc_apply(const kz_lrc* h, int32_t op, int32_t b, const double* in1, const double* in2,
+                 double* out, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- K4: batched masked top-k --------------------------------------------
  * For each column j of scores (device double[b][n], entries >= 0) select the
  * k entries with the largest (score desc, id asc) key among ids that are not

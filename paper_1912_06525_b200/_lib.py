@@ -89,29 +89,32 @@ class KzLrcDesc(ctypes.Structure):
         ("n2", ctypes.c_int64),
         ("ell", ctypes.c_int64),
         ("beta", ctypes.c_double),
-        ("a_rowptr", ctypes.c_void_p),
-        ("a_colidx", ctypes.c_void_p),
-        ("a_nnz", ctypes.c_int64),
-        ("num_parts", ctypes.c_int64),
-        ("part_ptr", ctypes.c_void_p),
-        ("part_inv", ctypes.c_void_p),
-        ("part_inv_off", ctypes.c_void_p),
+        ("full", ctypes.c_void_p),
+        ("a12", ctypes.c_void_p),
+        ("a21", ctypes.c_void_p),
+        ("a22", ctypes.c_void_p),
+        ("minv", ctypes.c_void_p),
         ("linv", ctypes.c_void_p),
+        ("linvT", ctypes.c_void_p),
         ("u", ctypes.c_void_p),
-        ("sigma", ctypes.c_void_p),
+        ("udT", ctypes.c_void_p),
+        ("sigma", ctypes.POINTER(ctypes.c_double)),
     ]
 
 
 class KzLrcArgs(ctypes.Structure):
     _fields_ = [
         ("b", ctypes.c_int32),
+        ("chunk", ctypes.c_int32),
         ("clamp", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
         ("qpos", ctypes.POINTER(ctypes.c_int64)),
+        ("f", ctypes.c_void_p),
         ("tol", ctypes.c_double),
         ("max_iter", ctypes.c_int64),
         ("x0", ctypes.c_void_p),
         ("perm", ctypes.c_void_p),
-        ("scores", ctypes.c_void_p),
+        ("out", ctypes.c_void_p),
         ("reports", ctypes.POINTER(KzReport)),
         ("device_ms", ctypes.POINTER(ctypes.c_float)),
     ]
@@ -161,17 +164,14 @@ def _declare(lib):
     lib.kz_coldot.argtypes = [i64, i32, vp, vp, vp, vp]
     lib.kz_profile_gather.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp, i32, vp]
     lib.kz_pearson_rerank.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp]
-    if hasattr(lib, "kz_lrc_create"):
-        lib.kz_lrc_create.argtypes = [c.POINTER(KzLrcDesc), c.POINTER(vp)]
-        lib.kz_lrc_destroy.argtypes = [vp]
-        lib.kz_lrc_info.argtypes = [vp, c.POINTER(i64), c.POINTER(i64), c.POINTER(i64), c.POINTER(i64)]
-        lib.kz_lrc_workspace_bytes.argtypes = [vp, i32]
-        lib.kz_lrc_workspace_bytes.restype = sz
-        lib.kz_lrc_batch.argtypes = [vp, c.POINTER(KzLrcArgs), vp, sz, vp]
-        lib.kz_lrc_apply_schur.argtypes = [vp, i32, vp, vp, vp, sz, vp]
-        lib.kz_lrc_apply_precond.argtypes = [vp, i32, vp, vp, vp, sz, vp]
-        lib.kz_lrc_schur_rhs.argtypes = [vp, i32, vp, vp, vp, vp, sz, vp]
-        lib.kz_dense_matmul.argtypes = [i64, i64, i64, dbl, vp, i64, i32, vp, i64, i32, dbl, vp, i64, i32, vp]
+    lib.kz_graph_create_weighted.argtypes = [i64, i64, i64, vp, vp, vp, c.POINTER(vp)]
+    lib.kz_lrc_create.argtypes = [c.POINTER(KzLrcDesc), c.POINTER(vp)]
+    lib.kz_lrc_destroy.argtypes = [vp]
+    lib.kz_lrc_info.argtypes = [vp, c.POINTER(i64), c.POINTER(i64), c.POINTER(i64), c.POINTER(i64)]
+    lib.kz_lrc_workspace_bytes.argtypes = [vp, i32, i32]
+    lib.kz_lrc_workspace_bytes.restype = sz
+    lib.kz_lrc_batch.argtypes = [vp, c.POINTER(KzLrcArgs), vp, sz, vp]
+    lib.kz_lrc_apply.argtypes = [vp, i32, i32, vp, vp, vp, vp, sz, vp]
 
 
 def error_from_status(code, lib=None):

@@ -185,10 +185,12 @@ __device__ __forceinline__ bool chunk_last_reduce(const RedScratch& rs, int chun
 template <int C>
 __global__ void __launch_bounds__(kThreads)
     coldot_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows,
-                  RedScratch red, int mode, SolveState s, double* out, int iter) {
+                  int64_t ldx, int64_t ldy, RedScratch red, int mode, SolveState s, double* out,
+                  int iter) {
     constexpr int VEC = Cfg<C>::VEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
-    const size_t base = static_cast<size_t>(chunk) * rows * C;
+    const double* Xb = X + static_cast<size_t>(chunk) * ldx;
+    const double* Yb = Y + static_cast<size_t>(chunk) * ldy;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
     const size_t stride = static_cast<size_t>(red.nb) * kThreads;
     double acc[VEC];
@@ -196,8 +198,8 @@ __global__ void __launch_bounds__(kThreads)
     for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
     for (size_t pi = static_cast<size_t>(local) * kThreads + threadIdx.x; pi < npairs; pi += stride) {
         double x[VEC], y[VEC];
-        ld_plain<VEC>(X + base + pi * VEC, x);
-        ld_plain<VEC>(Y + base + pi * VEC, y);
+        ld_plain<VEC>(Xb + pi * VEC, x);
+        ld_plain<VEC>(Yb + pi * VEC, y);
 #pragma unroll
         for (int q = 0; q < VEC; ++q) acc[q] = fma(x[q], y[q], acc[q]);
     }
@@ -213,11 +215,12 @@ __global__ void __launch_bounds__(kThreads)
 template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_update_kernel(double* __restrict__ r, const double* __restrict__ q, int64_t rows,
-                     RedScratch red, int mode, SolveState s, int iter) {
+                     int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter) {
     constexpr int VEC = Cfg<C>::VEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
     if (s.chunk_xstamp[chunk] != iter) return;
-    const size_t base = static_cast<size_t>(chunk) * rows * C;
+    r += static_cast<size_t>(chunk) * ldr;
+    q += static_cast<size_t>(chunk) * ldq;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
     const size_t stride = static_cast<size_t>(red.nb) * kThreads;
     const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
@@ -235,14 +238,14 @@ __global__ void __launch_bounds__(kThreads)
     for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
     for (size_t pi = t0; pi < npairs; pi += stride) {
         double rv[VEC], qv[VEC];
-        ld_plain<VEC>(r + base + pi * VEC, rv);
-        ld_plain<VEC>(q + base + pi * VEC, qv);
+        ld_plain<VEC>(r + pi * VEC, rv);
+        ld_plain<VEC>(q + pi * VEC, qv);
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
             if (on[k]) rv[k] = __dsub_rn(rv[k], __dmul_rn(a[k], qv[k]));
             acc[k] = fma(rv[k], rv[k], acc[k]);
         }
-        st_plain<VEC>(r + base + pi * VEC, rv);
+        st_plain<VEC>(r + pi * VEC, rv);
     }
     __shared__ double sm[kThreads];
     const double mine = block_col_reduce<C, VEC>(acc, sm);
@@ -257,11 +260,14 @@ __global__ void __launch_bounds__(kThreads)
 template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_pupdate_kernel(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ d,
-                      int64_t rows, int nb, SolveState s, int iter) {
+                      int64_t rows, int64_t ldx, int64_t ldp, int64_t ldd, int nb, SolveState s,
+                      int iter) {
     constexpr int VEC = Cfg<C>::VEC;
     const int chunk = blockIdx.x / nb, local = blockIdx.x - chunk * nb;
     if (s.chunk_xstamp[chunk] != iter) return;
-    const size_t base = static_cast<size_t>(chunk) * rows * C;
+    x += static_cast<size_t>(chunk) * ldx;
+    p += static_cast<size_t>(chunk) * ldp;
+    d += static_cast<size_t>(chunk) * ldd;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
     const size_t stride = static_cast<size_t>(nb) * kThreads;
     const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
@@ -278,23 +284,23 @@ __global__ void __launch_bounds__(kThreads)
     }
     for (size_t pi = t0; pi < npairs; pi += stride) {
         double xv[VEC], pv[VEC], dv[VEC];
-        ld_plain<VEC>(x + base + pi * VEC, xv);
-        ld_plain<VEC>(p + base + pi * VEC, pv);
-        ld_plain<VEC>(d + base + pi * VEC, dv);
+        ld_plain<VEC>(x + pi * VEC, xv);
+        ld_plain<VEC>(p + pi * VEC, pv);
+        ld_plain<VEC>(d + pi * VEC, dv);
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
             if (ox[k]) xv[k] = __dadd_rn(xv[k], __dmul_rn(a[k], pv[k]));
             if (op[k]) pv[k] = __dadd_rn(dv[k], __dmul_rn(bc[k], pv[k]));
         }
-        st_plain<VEC>(x + base + pi * VEC, xv);
-        st_plain<VEC>(p + base + pi * VEC, pv);
+        st_plain<VEC>(x + pi * VEC, xv);
+        st_plain<VEC>(p + pi * VEC, pv);
     }
 }
 
 // rhs of query column j: beta * A[:, qpos[j]] (index.py:93-101), written into
 // a zeroed block.  One CTA per column walks CSR row qpos[j] (A symmetric).
 template <int C>
-__global__ void scatter_rhs_kernel(double* __restrict__ r, int64_t rows,
+__global__ void scatter_rhs_kernel(double* __restrict__ r, int64_t ld,
                                    const int32_t* __restrict__ rowptr,
                                    const int32_t* __restrict__ colidx,
                                    const int64_t* __restrict__ qpos, int b, double beta) {
@@ -303,13 +309,13 @@ __global__ void scatter_rhs_kernel(double* __restrict__ r, int64_t rows,
     const int64_t q = qpos[j];
     const int beg = rowptr[q], end = rowptr[q + 1];
     for (int k = beg + threadIdx.x; k < end; k += blockDim.x)
-        r[blk_index(rows, C, colidx[k], j)] = beta;
+        r[static_cast<size_t>(j / C) * ld + static_cast<size_t>(colidx[k]) * C + (j % C)] = beta;
 }
 
 // column-major [b][rows] -> chunked block (tile transpose through shared memory)
 template <int C>
 __global__ void load_colmajor_kernel(double* __restrict__ dst, const double* __restrict__ src,
-                                     int64_t rows, int b, int nchunks) {
+                                     int64_t rows, int64_t ld, int b, int nchunks) {
     constexpr int TR = 64;
     __shared__ double sm[TR * (C + 1)];
     const int64_t ntiles = (rows + TR - 1) / TR;
@@ -326,7 +332,7 @@ __global__ void load_colmajor_kernel(double* __restrict__ dst, const double* __r
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
             const int rr = e / C, c = e % C;
             const int64_t row = r0 + rr;
-            if (row < rows) dst[(static_cast<size_t>(chunk) * rows + row) * C + c] = sm[rr * (C + 1) + c];
+            if (row < rows) dst[static_cast<size_t>(chunk) * ld + static_cast<size_t>(row) * C + c] = sm[rr * (C + 1) + c];
         }
         __syncthreads();
     }
@@ -336,7 +342,7 @@ __global__ void load_colmajor_kernel(double* __restrict__ dst, const double* __r
 // the clamp at zero (solver.py:181-184, 223-225).
 template <int C>
 __global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __restrict__ src,
-                                      int64_t rows, int b, int nchunks,
+                                      int64_t rows, int64_t ld, int b, int nchunks,
                                       const int64_t* __restrict__ perm, int clamp) {
     constexpr int TR = 64;
     __shared__ double sm[TR * (C + 1)];
@@ -347,7 +353,7 @@ __global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
             const int rr = e / C, c = e % C;
             const int64_t row = r0 + rr;
-            sm[rr * (C + 1) + c] = row < rows ? src[(static_cast<size_t>(chunk) * rows + row) * C + c] : 0.0;
+            sm[rr * (C + 1) + c] = row < rows ? src[static_cast<size_t>(chunk) * ld + static_cast<size_t>(row) * C + c] : 0.0;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
@@ -367,7 +373,7 @@ __global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __
 
 template <int C>
 __global__ void broadcast_kernel(double* __restrict__ dst, const double* __restrict__ v,
-                                 int64_t rows, int b, int nchunks) {
+                                 int64_t rows, int64_t ld, int b, int nchunks) {
     const size_t total = static_cast<size_t>(nchunks) * rows * C;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -375,7 +381,7 @@ __global__ void broadcast_kernel(double* __restrict__ dst, const double* __restr
         const size_t rowc = e / C;
         const int chunk = static_cast<int>(rowc / rows);
         const int64_t row = static_cast<int64_t>(rowc - static_cast<size_t>(chunk) * rows);
-        dst[e] = (chunk * C + c < b) ? v[row] : 0.0;
+        dst[static_cast<size_t>(chunk) * ld + static_cast<size_t>(row) * C + c] = (chunk * C + c < b) ? v[row] : 0.0;
     }
 }
 

@@ -126,20 +126,20 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
 
     // right-hand side
     if (a->rhs) {
-        KZ_DISPATCH_C(C, load_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.r, a->rhs, n, b, nchunks); ::kz::note_launch());
+        KZ_DISPATCH_C(C, load_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.r, a->rhs, n, n * CC, b, nchunks); ::kz::note_launch());
     } else {
         KZ_CUDA(cudaMemsetAsync(w.r, 0, blk_bytes, st));
         KZ_CUDA(cudaMemcpyAsync(w.qpos, a->qpos, sizeof(int64_t) * b, cudaMemcpyHostToDevice, st));
-        KZ_DISPATCH_C(C, scatter_rhs_kernel<CC><<<b, kThreads, 0, st>>>(w.r, n, g->rowptr, g->colidx, w.qpos, b, a->beta); ::kz::note_launch());
+        KZ_DISPATCH_C(C, scatter_rhs_kernel<CC><<<b, kThreads, 0, st>>>(w.r, n * CC, g->rowptr, g->colidx, w.qpos, b, a->beta); ::kz::note_launch());
     }
     KZ_LAUNCH_CHECK();
     // ||b||, optional start vector (solver.py:51-59), init finalize
-    KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, w.red,
+    KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red,
                                                                      a->x0 ? FIN_INIT_B : FIN_INIT_BR,
                                                                      s, nullptr, 0); ::kz::note_launch());
     KZ_LAUNCH_CHECK();
     if (a->x0) {
-        KZ_DISPATCH_C(C, broadcast_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.x, a->x0, n, b, nchunks); ::kz::note_launch());
+        KZ_DISPATCH_C(C, broadcast_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.x, a->x0, n, n * CC, b, nchunks); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
         SpmmArgs sa = make_spmm_args(g, w.sp);
         sa.Xg = w.x;
@@ -151,7 +151,7 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
         sa.s2 = a->beta;  // r = b - (x - beta*A x)
         sa.want_dot = 0;
         if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
-        KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
+        KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
     }
     KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));
@@ -182,9 +182,9 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
         sa.hook.n_active = s.n_active;
         sa.hook.iter = k;
         if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
-        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, w.red, FIN_CG_CONV, s, k); ::kz::note_launch());
+        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
-        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, w.r, n, nb, s, k); ::kz::note_launch());
+        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, w.r, n, n * CC, n * CC, n * CC, nb, s, k); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
         return KZ_OK;
     };
@@ -192,7 +192,7 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
     int rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
     if (rc) return rc;
 
-    KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, b, nchunks, a->perm, a->clamp); ::kz::note_launch());
+    KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, a->perm, a->clamp); ::kz::note_launch());
     KZ_LAUNCH_CHECK();
     if (a->device_ms) {
         KZ_CUDA(cudaEventRecord(e1, st));
@@ -256,7 +256,7 @@ extern "C" int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y,
     red.cnt = cnt;
     KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * b, st));
     SolveState s;
-    coldot_kernel<1><<<static_cast<unsigned>(b) * nb, kThreads, 0, st>>>(X, Y, n, red, FIN_WRITE, s, out, 0); ::kz::note_launch();
+    coldot_kernel<1><<<static_cast<unsigned>(b) * nb, kThreads, 0, st>>>(X, Y, n, n, n, red, FIN_WRITE, s, out, 0); ::kz::note_launch();
     KZ_LAUNCH_CHECK();
     return KZ_OK;
 }

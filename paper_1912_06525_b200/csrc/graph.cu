@@ -41,20 +41,86 @@ void free_graph(kz_graph* g) {
     if (!g) return;
     cudaFree(g->rowptr);
     cudaFree(g->colidx);
-    cudaFree(g->long_rows);
-    cudaFree(g->long_first);
-    cudaFree(g->item_lrow);
-    cudaFree(g->cta_rows);
-    cudaFree(g->cta_long);
+    cudaFree(g->vals);
+    cudaFree(g->tasks);
+    cudaFree(g->cta_task);
+    cudaFree(g->long_seg0);
     delete g;
+}
+
+// Host schedule for K1 (see spmm.cuh): warp tasks in row order and
+// cost-balanced contiguous task ranges per CTA.
+void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<int4>& tasks,
+                    std::vector<int32_t>& cta_task, std::vector<int32_t>& long_seg0, int32_t& max_deg) {
+    std::vector<double> cost;
+    int64_t s_open = -1, s_rows = 0;
+    double s_cost = 0.0;
+    auto close_s = [&](int64_t end) {
+        if (s_open >= 0) {
+            tasks.push_back(make_int4(static_cast<int>(s_open), static_cast<int>(end), TASK_S, 0));
+            cost.push_back(s_cost);
+            s_open = -1;
+        }
+    };
+    int32_t nlong = 0, nseg = 0;
+    max_deg = 0;
+    for (int64_t i = 0; i < rows; ++i) {
+        const int64_t d = rp[i + 1] - rp[i];
+        max_deg = std::max<int32_t>(max_deg, static_cast<int32_t>(d));
+        if (d <= kMedDeg) {
+            if (s_open >= 0 && (s_rows >= 32 || s_cost + d + 4 > 256.0)) close_s(i);
+            if (s_open < 0) {
+                s_open = i;
+                s_rows = 0;
+                s_cost = 0.0;
+            }
+            s_rows += 1;
+            s_cost += d + 4.0;
+        } else if (d <= kSegLen) {
+            close_s(i);
+            tasks.push_back(make_int4(static_cast<int>(i), 0, TASK_M, 0));
+            cost.push_back(d + 8.0);
+        } else {
+            close_s(i);
+            const int64_t ns = (d + kSegLen - 1) / kSegLen;
+            long_seg0.push_back(nseg);
+            for (int64_t k = 0; k < ns; ++k) {
+                tasks.push_back(make_int4(static_cast<int>(i), nlong, TASK_L, static_cast<int>(k)));
+                cost.push_back(std::min<double>(kSegLen, d - k * kSegLen) + 8.0);
+            }
+            nseg += static_cast<int32_t>(ns);
+            ++nlong;
+        }
+    }
+    close_s(rows);
+    long_seg0.push_back(nseg);
+    double total = 0.0;
+    for (double c : cost) total += c;
+    const double target = std::max(256.0, std::min(16384.0, total / (2.0 * kNumSMs)));
+    cta_task.push_back(0);
+    double acc = 0.0;
+    int cnt = 0;
+    for (size_t t = 0; t < tasks.size(); ++t) {
+        if (cnt > 0 && (acc + cost[t] > target || cnt >= kTaskCap)) {
+            cta_task.push_back(static_cast<int32_t>(t));
+            acc = 0.0;
+            cnt = 0;
+        }
+        acc += cost[t];
+        ++cnt;
+    }
+    if (tasks.empty() || cta_task.back() != static_cast<int32_t>(tasks.size()))
+        cta_task.push_back(static_cast<int32_t>(tasks.size()));
 }
 
 }  // namespace
 
-// Builds the SpMM schedule on the host from rowptr (rows+1 ints): long-row
-// segments and cost-balanced row ranges per CTA.
-extern "C" int kz_graph_create(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
-                               const int32_t* colidx, kz_graph** out) {
+namespace kz {
+
+// Creates an operator handle; vals (host or device, nnz doubles) makes it a
+// weighted operator (used for the block-diagonal M11^-1 of the LRC path).
+int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
+                 const int32_t* colidx, const double* vals, kz_graph** out) {
     clear_error();
     if (!out) return fail(KZ_EARG, "out is NULL");
     *out = nullptr;
@@ -77,77 +143,49 @@ extern "C" int kz_graph_create(int64_t rows, int64_t cols, int64_t nnz, const in
     g->rows = rows;
     g->cols = cols;
     g->nnz = nnz;
-    const int64_t seg = g->seg;
-
-    std::vector<int32_t> rp32(rows + 1), long_rows, long_first, item_lrow;
-    std::vector<double> cost_prefix(rows + 1, 0.0);
-    int32_t max_deg = 0;
-    for (int64_t i = 0; i < rows; ++i) {
-        rp32[i] = static_cast<int32_t>(rp[i]);
-        const int64_t d = rp[i + 1] - rp[i];
-        max_deg = std::max<int32_t>(max_deg, static_cast<int32_t>(d));
-        double c;
-        if (d > seg) {
-            const int64_t ns = (d + seg - 1) / seg;
-            long_first.push_back(static_cast<int32_t>(item_lrow.size()));
-            for (int64_t s = 0; s < ns; ++s) item_lrow.push_back(static_cast<int32_t>(long_rows.size()));
-            long_rows.push_back(static_cast<int32_t>(i));
-            c = 8.0 + static_cast<double>(ns);
-        } else {
-            c = 4.0 + static_cast<double>(d);
-        }
-        cost_prefix[i + 1] = cost_prefix[i] + c;
-    }
-    rp32[rows] = static_cast<int32_t>(rp[rows]);
-    long_first.push_back(static_cast<int32_t>(item_lrow.size()));
-    g->max_deg = max_deg;
-    g->nlong = static_cast<int32_t>(long_rows.size());
-    g->nitems = static_cast<int32_t>(item_lrow.size());
-
-    // row-range CTAs: about 1 KB-of-index of work each, at most one resident wave per chunk
-    const double total = cost_prefix[rows];
-    int64_t nshort = static_cast<int64_t>(total / 512.0) + 1;
-    nshort = std::max<int64_t>(1, std::min<int64_t>(nshort, kMaxCtasPerChunk));
-    nshort = std::min<int64_t>(nshort, rows);
-    std::vector<int32_t> cta_rows(nshort + 1), cta_long(nshort + 1);
-    cta_rows[0] = 0;
-    for (int64_t p = 1; p < nshort; ++p) {
-        const double target = total * static_cast<double>(p) / static_cast<double>(nshort);
-        int64_t r = std::lower_bound(cost_prefix.begin(), cost_prefix.end(), target) - cost_prefix.begin();
-        r = std::max<int64_t>(r, cta_rows[p - 1]);
-        r = std::min<int64_t>(r, rows);
-        cta_rows[p] = static_cast<int32_t>(r);
-    }
-    cta_rows[nshort] = static_cast<int32_t>(rows);
-    for (int64_t p = 0; p <= nshort; ++p)
-        cta_long[p] = static_cast<int32_t>(
-            std::lower_bound(long_rows.begin(), long_rows.end(), cta_rows[p]) - long_rows.begin());
-    g->nshort = static_cast<int32_t>(nshort);
-    g->nlongcta = g->nitems == 0
-                      ? 0
-                      : static_cast<int32_t>(std::min<int64_t>(
-                            kMaxCtasPerChunk, std::max<int64_t>(1, (g->nitems + 4 * kWarps - 1) / (4 * kWarps))));
+    std::vector<int32_t> rp32(rows + 1);
+    for (int64_t i = 0; i <= rows; ++i) rp32[i] = static_cast<int32_t>(rp[i]);
+    std::vector<int4> tasks;
+    std::vector<int32_t> cta_task, long_seg0;
+    build_schedule(rp, rows, tasks, cta_task, long_seg0, g->max_deg);
+    g->ntasks = static_cast<int32_t>(tasks.size());
+    g->ncta = static_cast<int32_t>(cta_task.size()) - 1;
+    g->nlong = static_cast<int32_t>(long_seg0.size()) - 1;
+    g->nseg = long_seg0.back();
 
     int st = KZ_OK;
     if ((st = upload(&g->rowptr, rp32.data(), rows + 1)) ||
         (st = upload(&g->colidx, static_cast<const int32_t*>(nullptr), nnz)) ||
-        (st = upload(&g->long_rows, long_rows.data(), long_rows.size())) ||
-        (st = upload(&g->long_first, long_first.data(), long_first.size())) ||
-        (st = upload(&g->item_lrow, item_lrow.data(), item_lrow.size())) ||
-        (st = upload(&g->cta_rows, cta_rows.data(), cta_rows.size())) ||
-        (st = upload(&g->cta_long, cta_long.data(), cta_long.size()))) {
+        (st = upload(&g->tasks, tasks.data(), tasks.size())) ||
+        (st = upload(&g->cta_task, cta_task.data(), cta_task.size())) ||
+        (st = upload(&g->long_seg0, long_seg0.data(), long_seg0.size())) ||
+        (vals && (st = upload(&g->vals, static_cast<const double*>(nullptr), nnz)))) {
         free_graph(g);
         return st;
     }
     if (nnz > 0) {
         cudaError_t e = cudaMemcpy(g->colidx, colidx, sizeof(int32_t) * nnz, cudaMemcpyDefault);
+        if (e == cudaSuccess && vals) e = cudaMemcpy(g->vals, vals, sizeof(double) * nnz, cudaMemcpyDefault);
         if (e != cudaSuccess) {
             free_graph(g);
-            return fail(KZ_ECUDA, std::string("colidx copy: ") + cudaGetErrorString(e));
+            return fail(KZ_ECUDA, std::string("CSR copy: ") + cudaGetErrorString(e));
         }
     }
     *out = g;
     return KZ_OK;
+}
+
+}  // namespace kz
+
+extern "C" int kz_graph_create(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
+                               const int32_t* colidx, kz_graph** out) {
+    return create_graph(rows, cols, nnz, rowptr, colidx, nullptr, out);
+}
+
+extern "C" int kz_graph_create_weighted(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
+                                        const int32_t* colidx, const double* vals, kz_graph** out) {
+    if (!vals && nnz > 0) return fail(KZ_EARG, "NULL values");
+    return create_graph(rows, cols, nnz, rowptr, colidx, vals, out);
 }
 
 extern "C" int kz_graph_destroy(kz_graph* g) {
@@ -162,7 +200,7 @@ extern "C" int kz_graph_info(const kz_graph* g, int64_t* rows, int64_t* cols, in
     if (cols) *cols = g->cols;
     if (nnz) *nnz = g->nnz;
     if (nlong) *nlong = g->nlong;
-    if (nitems) *nitems = g->nitems;
+    if (nitems) *nitems = g->nseg;
     return KZ_OK;
 }
 

@@ -5,47 +5,59 @@
 //
 // Replaces the reference's operator applications: KatzIndex.apply_m_permuted
 // (index.py:86-91: x - alpha*A x through factor reassembly), the coupling
-// products m12 @ v / m12.T @ u (solver.py:110,115,178) and the rhs column
+// products m12 @ v / m12.T @ u (solver.py:110,115,178), the interior solve
+// M11^-1 (factor.py:89-106, as a weighted operator) and the rhs column
 // (index.py:93-101).  A is a binary pattern (no stored values, int32 column
 // indices), so the only per-nonzero traffic is 4 bytes of index plus a
 // gathered C-wide row segment of Xg.
 //
-// Layout: blocks are chunked node-major [b/C][rows][C] (C doubles of one row
-// are contiguous, 16*C bytes... i.e. 8*C bytes), so one gathered neighbour is a
-// coalesced 8*C-byte segment read by G = C/VEC lanes with 16-byte vector
-// loads.  The grid is chunk-major, so at any moment the L2 working set is
-// one chunk of Xg (rows*8*C bytes) rather than the whole block.
+// Layout: blocks are chunked node-major [b/C][rows][C] (the C doubles of one
+// row are contiguous, 8*C bytes), so a gathered neighbour is one coalesced
+// segment read by G = C/VEC lanes with 16-byte loads.  The grid is
+// chunk-major, so the L2 working set is one chunk of Xg, not the block.
 //
-// Power-law degree skew: rows with deg <= seg ("short") are handled by one
-// lane group each, in CSR order, so their sum is bit-identical to scipy's
-// csr_matvec.  Longer rows are cut into seg-long segments processed by whole
-// warps in dedicated CTAs (launched first in each chunk); their partial sums
-// are combined in a fixed order by the CTA that owns the row's range, which
-// waits on a per-row completion counter (stream-K style fix-up).  All dot
-// partials are reduced in a fixed order by the last CTA of the chunk, so the
-// result is run-to-run deterministic.
+// Schedule (built once per operator on the host, graph.cu): the rows are cut
+// into warp tasks in row order --
+//   S  a run of short rows (deg <= kMedDeg), one lane group per row;
+//   M  one medium row, its neighbours split over the warp's lane groups;
+//   L  one kSegLen-long segment of a long row (power-law hubs); the warp that
+//      runs a row's last segment waits for the others and combines the
+//      partial sums in segment order (stream-K style fix-up).
+// Each CTA owns a contiguous task range and its warps pull tasks dynamically
+// (no intra-CTA tail); every task's dot partial lands in its own shared slot
+// and slots are summed in task order, then CTAs in CTA order by the last CTA
+// of the chunk, so the column dots are run-to-run deterministic.  Short and
+// medium rows sum their neighbours in CSR order with explicit _rn adds, so
+// they are bit-identical to scipy's csr_matvec.
 #pragma once
 
 #include "common.cuh"
+
+namespace kz {
+constexpr int kMedDeg = 32;      // rows with deg <= kMedDeg are "short"
+constexpr int kSegLen = 1024;    // rows with deg > kSegLen are split into segments
+constexpr int kTaskCap = 128;    // max tasks per CTA (dot slots in shared memory)
+constexpr int kSpmmMinBlocks = 2;
+}  // namespace kz
 
 struct kz_graph {
     int64_t rows = 0, cols = 0, nnz = 0;
     int32_t* rowptr = nullptr;  // device int32[rows+1]
     int32_t* colidx = nullptr;  // device int32[nnz]
-    int32_t seg = 512;          // long-row segment length
-    int32_t nlong = 0;          // rows with degree > seg
-    int32_t nitems = 0;         // seg-long segments of the long rows
-    int32_t* long_rows = nullptr;   // [nlong] sorted row ids
-    int32_t* long_first = nullptr;  // [nlong+1] first segment of each long row
-    int32_t* item_lrow = nullptr;   // [nitems] owning long-row index
-    int32_t nshort = 0;             // row-range CTAs per chunk
-    int32_t* cta_rows = nullptr;    // [nshort+1] row ranges (cost balanced)
-    int32_t* cta_long = nullptr;    // [nshort+1] long-row index ranges per CTA
-    int32_t nlongcta = 0;           // segment CTAs per chunk
+    double* vals = nullptr;     // optional fp64 values (weighted operator, e.g. M11^-1)
+    int32_t ntasks = 0;
+    int4* tasks = nullptr;      // {a, b, type, k}: S {r0, r1}, M {row}, L {row, lidx, seg k}
+    int32_t ncta = 0;           // CTAs per chunk
+    int32_t* cta_task = nullptr;    // [ncta+1] task ranges
+    int32_t nlong = 0;              // rows with deg > kSegLen
+    int32_t nseg = 0;               // their segments
+    int32_t* long_seg0 = nullptr;   // [nlong+1] first segment slot of each long row
     int32_t max_deg = 0;
 };
 
 namespace kz {
+
+enum TaskType : int { TASK_S = 0, TASK_M = 1, TASK_L = 2 };
 
 template <int C>
 struct Cfg {
@@ -89,38 +101,62 @@ __device__ __forceinline__ void st_plain(double* p, const double (&v)[VEC]) {
 
 // Sum Xg rows of neighbours col[beg..end) into acc, R neighbours per round,
 // rounds `stride` apart.  All lanes of a group share the neighbour; lane lg
-// owns columns lg*VEC .. lg*VEC+VEC-1 of the chunk.
-template <int C>
+// owns columns lg*VEC .. lg*VEC+VEC-1 of the chunk.  W: weighted operator.
+template <int C, bool W = false>
 __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int beg, int end,
                                             int stride, const double* __restrict__ Xc, int lg,
                                             int gbase, unsigned gmask,
-                                            double (&acc)[Cfg<C>::VEC]) {
+                                            double (&acc)[Cfg<C>::VEC],
+                                            const double* __restrict__ vals = nullptr) {
     using K = Cfg<C>;
+    // Software pipeline: the column indices of round k+1 are loaded while the
+    // R gathers of round k are in flight.  Tail slots gather a clamped valid
+    // row (index 0, always cache-hot) instead of predicating the load, so the
+    // compiler keeps all R loads outstanding; their sums are skipped.
+    int idx[K::PER], nidx[K::PER];
+    double wv[K::PER], nwv[K::PER];
+#pragma unroll
+    for (int m = 0; m < K::PER; ++m) {
+        const int pos = beg + lg + K::G * m;
+        nidx[m] = (pos < end) ? __ldg(col + pos) : 0;
+        if constexpr (W) nwv[m] = (pos < end) ? __ldg(vals + pos) : 0.0;
+    }
+    const double* __restrict__ Xl = Xc + lg * K::VEC;
+#pragma unroll 1
     for (int base = beg; base < end; base += stride) {
-        int idx[K::PER];
 #pragma unroll
         for (int m = 0; m < K::PER; ++m) {
-            const int pos = base + lg + K::G * m;
-            idx[m] = (pos < end) ? __ldg(col + pos) : -1;
+            idx[m] = nidx[m];
+            if constexpr (W) wv[m] = nwv[m];
+            const int pos = base + stride + lg + K::G * m;
+            nidx[m] = (pos < end) ? __ldg(col + pos) : 0;
+            if constexpr (W) nwv[m] = (pos < end) ? __ldg(vals + pos) : 0.0;
         }
         double v[K::R][K::VEC];
-        int jj[K::R];
+        double w[K::R];
 #pragma unroll
         for (int t = 0; t < K::R; ++t) {
             int j;
-            if constexpr (K::G == 1)
+            if constexpr (K::G == 1) {
                 j = idx[t];
-            else
+                if constexpr (W) w[t] = wv[t];
+            } else {
                 j = __shfl_sync(gmask, idx[t / K::G], gbase + (t % K::G));
-            jj[t] = j;
-            if (j >= 0)
-                ld_nc<K::VEC>(Xc + static_cast<size_t>(j) * C + lg * K::VEC, v[t]);
+                if constexpr (W) w[t] = __shfl_sync(gmask, wv[t / K::G], gbase + (t % K::G));
+            }
+            ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
         }
+        const int nvalid = end - base;  // slots t < nvalid hold real neighbours
 #pragma unroll
         for (int t = 0; t < K::R; ++t)
-            if (jj[t] >= 0) {
+            if (t < nvalid) {
 #pragma unroll
-                for (int q = 0; q < K::VEC; ++q) acc[q] = __dadd_rn(acc[q], v[t][q]);
+                for (int q = 0; q < K::VEC; ++q) {
+                    if constexpr (W)
+                        acc[q] = fma(w[t], v[t][q], acc[q]);
+                    else
+                        acc[q] = __dadd_rn(acc[q], v[t][q]);
+                }
             }
     }
 }
@@ -146,22 +182,23 @@ struct SpmmArgs {
     int32_t rows, cols;
     const int32_t* __restrict__ rowptr;
     const int32_t* __restrict__ colidx;
-    int32_t seg, nlong, nitems, nshort, nlongcta;
-    const int32_t* long_rows;
-    const int32_t* long_first;
-    const int32_t* item_lrow;
-    const int32_t* cta_rows;
-    const int32_t* cta_long;
+    const int4* __restrict__ tasks;
+    const int32_t* __restrict__ cta_task;
+    const int32_t* __restrict__ long_seg0;
+    int32_t ncta, nlong, nseg;
     const double* Xg;
     const double* Xs;
     const double* Z;
     double* Y;
     const double* D;
+    // chunk strides (elements) of each operand; 0 = dense default (rows*C or cols*C)
+    int64_t ldxg, ldxs, ldz, ldy, ldd;
+    const double* vals;  // weighted operator values (nullptr: binary pattern)
     double s0, s1, s2;
-    double* partial;
-    int32_t* rowcnt;
-    double* dotcta;
-    int32_t* chunkcnt;
+    double* partial;   // [nchunks][nseg][C] long-row segment sums
+    int32_t* rowcnt;   // [nchunks][nlong] finished-segment counters
+    double* dotcta;    // [nchunks][ncta][C]
+    int32_t* chunkcnt; // [nchunks]
     const int32_t* chunk_active;  // optional per-chunk skip flags
     int32_t want_dot;
     DotHook hook;
@@ -206,65 +243,32 @@ __device__ __forceinline__ void apply_dot_hook(const DotHook& h, int col, double
     }
 }
 
-template <int C>
-__global__ void __launch_bounds__(kThreads) spmm_kernel(SpmmArgs a) {
+template <int C, bool W>
+__global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs a) {
     using K = Cfg<C>;
     constexpr int VEC = K::VEC;
-    const int per_chunk = a.nlongcta + a.nshort;
-    const int chunk = blockIdx.x / per_chunk;
-    const int local = blockIdx.x - chunk * per_chunk;
+    const int chunk = blockIdx.x / a.ncta;
+    const int p = blockIdx.x - chunk * a.ncta;
     if (a.chunk_active && !a.chunk_active[chunk]) return;
 
+    __shared__ double slot[kTaskCap * C];
+    __shared__ double sm[kThreads];
+    __shared__ int next_task;
+    __shared__ int is_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = lane / K::G, lg = lane % K::G, gbase = gw * K::G;
     const unsigned gmask = (K::G == 32) ? 0xffffffffu : (((1u << K::G) - 1u) << gbase);
-    const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.cols * C;
+    const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.ldxg;
+    const int t0 = a.cta_task[p], nt = a.cta_task[p + 1] - t0;
+    if (threadIdx.x == 0) next_task = 0;
+    __syncthreads();
 
-    if (local < a.nlongcta) {
-        // ---- long-row segments: one warp per segment, partial sums out ----
-        const int nw_total = a.nlongcta * kWarps;
-        for (int it = local * kWarps + warp; it < a.nitems; it += nw_total) {
-            const int lr = a.item_lrow[it];
-            const int row = a.long_rows[lr];
-            const int k = it - a.long_first[lr];
-            const int beg = a.rowptr[row] + k * a.seg;
-            const int end = min(beg + a.seg, a.rowptr[row + 1]);
-            double acc[VEC];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-            gather_rows<C>(a.colidx, beg + gw * K::R, end, K::NGW * K::R, Xc, lg, gbase, gmask,
-                           acc);
-#pragma unroll
-            for (int off = K::G; off < 32; off <<= 1)
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
-            if (lane < K::G) {
-                st_plain<VEC>(a.partial + (static_cast<size_t>(chunk) * a.nitems + it) * C +
-                                  lg * VEC,
-                              acc);
-                __threadfence();
-            }
-            __syncwarp();
-            if (lane == 0) atomicAdd(a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lr, 1);
-        }
-        return;
-    }
-
-    // ---- row-range CTA: short rows by lane groups, then owned long rows ----
-    const int p = local - a.nlongcta;
-    const int rb = a.cta_rows[p], re = a.cta_rows[p + 1];
-    const int ngroups = kWarps * K::NGW;
-    const int gid = warp * K::NGW + gw;
-    double dacc[VEC];
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) dacc[q] = 0.0;
-
-    auto epilogue = [&](int row, const double (&acc)[VEC]) {
-        const size_t off = (static_cast<size_t>(chunk) * a.rows + row) * C + lg * VEC;
+    auto epilogue = [&](int row, const double (&acc)[VEC], double (&dacc)[VEC]) {
+        const size_t roff = static_cast<size_t>(row) * C + lg * VEC;
         double y[VEC];
         if (a.Xs) {
             double xs[VEC];
-            ld_plain<VEC>(a.Xs + off, xs);
+            ld_plain<VEC>(a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, xs);
 #pragma unroll
             for (int q = 0; q < VEC; ++q)
                 y[q] = __dadd_rn(__dmul_rn(a.s1, xs[q]), __dmul_rn(a.s2, acc[q]));
@@ -274,89 +278,121 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpmmArgs a) {
         }
         if (a.Z) {
             double z[VEC];
-            ld_plain<VEC>(a.Z + off, z);
+            ld_plain<VEC>(a.Z + static_cast<size_t>(chunk) * a.ldz + roff, z);
 #pragma unroll
             for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(a.s0, z[q]), y[q]);
         }
-        st_plain<VEC>(a.Y + off, y);
+        st_plain<VEC>(a.Y + static_cast<size_t>(chunk) * a.ldy + roff, y);
         if (a.want_dot) {
             double d[VEC];
-            ld_plain<VEC>((a.D ? a.D : a.Xs) + off, d);
+            ld_plain<VEC>(a.D ? a.D + static_cast<size_t>(chunk) * a.ldd + roff
+                              : a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, d);
 #pragma unroll
             for (int q = 0; q < VEC; ++q) dacc[q] = fma(d[q], y[q], dacc[q]);
         }
     };
-
-    for (int row = rb + gid; row < re; row += ngroups) {
-        const int beg = a.rowptr[row], end = a.rowptr[row + 1];
-        if (end - beg > a.seg) continue;  // long row: finished below
-        double acc[VEC];
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-        gather_rows<C>(a.colidx, beg, end, K::R, Xc, lg, gbase, gmask, acc);
-        epilogue(row, acc);
-    }
-
-    // long rows whose range this CTA owns: wait for their segments, combine
-    // the partials in segment order, run the epilogue
-    const int l0 = a.cta_long[p], l1 = a.cta_long[p + 1];
-    for (int lr = l0 + warp; lr < l1; lr += kWarps) {
-        const int row = a.long_rows[lr];
-        const int f = a.long_first[lr], nseg = a.long_first[lr + 1] - f;
-        int* cnt = a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lr;
-        if (lane == 0) {
-            while (atomicAdd(cnt, 0) < nseg) __nanosleep(100);
-            __threadfence();
-        }
-        __syncwarp();
-        double acc[VEC];
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-        for (int s = gw; s < nseg; s += K::NGW) {
-            const double* src =
-                a.partial + (static_cast<size_t>(chunk) * a.nitems + f + s) * C + lg * VEC;
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] += __ldcg(src + q);
-        }
+    auto warp_sum = [&](double (&v)[VEC]) {
 #pragma unroll
         for (int off = K::G; off < 32; off <<= 1)
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
-        if (gw == 0) epilogue(row, acc);
-        __syncwarp();
-        if (lane == 0) *cnt = 0;  // re-arm for the next launch
+            for (int q = 0; q < VEC; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+    };
+
+    while (true) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&next_task, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= nt) break;
+        const int4 task = a.tasks[t0 + t];
+        double dacc[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) dacc[q] = 0.0;
+        if (task.z == TASK_S) {
+            for (int row = task.x + gw; row < task.y; row += K::NGW) {
+                double acc[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+                gather_rows<C, W>(a.colidx, a.rowptr[row], a.rowptr[row + 1], K::R, Xc, lg, gbase,
+                                  gmask, acc, a.vals);
+                epilogue(row, acc, dacc);
+            }
+        } else if (task.z == TASK_M) {
+            const int row = task.x;
+            double acc[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+            gather_rows<C, W>(a.colidx, a.rowptr[row] + gw * K::R, a.rowptr[row + 1], K::NGW * K::R,
+                              Xc, lg, gbase, gmask, acc, a.vals);
+            warp_sum(acc);
+            if (gw == 0) epilogue(row, acc, dacc);
+        } else {
+            // long-row segment k of long row lidx
+            const int row = task.x, lidx = task.y, k = task.w;
+            const int s0 = a.long_seg0[lidx], nseg = a.long_seg0[lidx + 1] - s0;
+            const int beg = a.rowptr[row] + k * kSegLen;
+            const int end = min(beg + kSegLen, a.rowptr[row + 1]);
+            double acc[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+            gather_rows<C, W>(a.colidx, beg + gw * K::R, end, K::NGW * K::R, Xc, lg, gbase, gmask,
+                              acc, a.vals);
+            warp_sum(acc);
+            double* pbase = a.partial + static_cast<size_t>(chunk) * a.nseg * C;
+            int* cnt = a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lidx;
+            if (k < nseg - 1) {
+                if (lane < K::G) {
+                    st_plain<VEC>(pbase + static_cast<size_t>(s0 + k) * C + lg * VEC, acc);
+                    __threadfence();
+                }
+                __syncwarp();
+                if (lane == 0) atomicAdd(cnt, 1);
+            } else {
+                // last segment: wait for the others, combine in segment order
+                if (lane == 0) {
+                    while (atomicAdd(cnt, 0) < nseg - 1) __nanosleep(64);
+                    __threadfence();
+                }
+                __syncwarp();
+                double tot[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) tot[q] = 0.0;
+                for (int s = 0; s < nseg - 1; ++s) {
+                    const double* src = pbase + static_cast<size_t>(s0 + s) * C + lg * VEC;
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) tot[q] += __ldcg(src + q);
+                }
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) tot[q] += acc[q];
+                if (gw == 0) epilogue(row, tot, dacc);
+                __syncwarp();
+                if (lane == 0) *cnt = 0;  // re-arm for the next launch
+            }
+        }
+        if (a.want_dot) {
+            warp_sum(dacc);
+            if (lane < K::G) {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) slot[t * C + lg * VEC + q] = dacc[q];
+            }
+        }
     }
 
     if (!a.want_dot) return;
-
-    // ---- deterministic column dots: warp -> CTA -> chunk ----
-#pragma unroll
-    for (int off = K::G; off < 32; off <<= 1)
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) dacc[q] += __shfl_xor_sync(0xffffffffu, dacc[q], off);
-    __shared__ double sm[kThreads];
-    __shared__ int is_last;
-    if (lane < K::G) {
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) sm[warp * C + lg * VEC + q] = dacc[q];
-    }
     __syncthreads();
+    // task slots in task order -> CTA partial -> last CTA of the chunk
     if (threadIdx.x < C) {
         double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s += sm[w * C + threadIdx.x];
-        a.dotcta[(static_cast<size_t>(chunk) * a.nshort + p) * C + threadIdx.x] = s;
+        for (int t = 0; t < nt; ++t) s += slot[t * C + threadIdx.x];
+        a.dotcta[(static_cast<size_t>(chunk) * a.ncta + p) * C + threadIdx.x] = s;
         __threadfence();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const int old = atomicAdd(a.chunkcnt + chunk, 1);
-        is_last = (old == a.nshort - 1);
-    }
+    if (threadIdx.x == 0) is_last = (atomicAdd(a.chunkcnt + chunk, 1) == a.ncta - 1);
     __syncthreads();
     if (!is_last) return;
     __threadfence();
     const double v =
-        reduce_partials<C>(a.dotcta + static_cast<size_t>(chunk) * a.nshort * C, a.nshort, sm);
+        reduce_partials<C>(a.dotcta + static_cast<size_t>(chunk) * a.ncta * C, a.ncta, sm);
     if (threadIdx.x < C) apply_dot_hook(a.hook, chunk * C + threadIdx.x, v, chunk);
     if (threadIdx.x == 0) {
         a.chunkcnt[chunk] = 0;
@@ -372,18 +408,38 @@ struct SpmmScratch {
     int32_t* chunkcnt = nullptr;
 };
 
-inline void carve_spmm_scratch(Carver& cv, const kz_graph* g, int nchunks, int C, SpmmScratch& s) {
-    s.partial = cv.take<double>(static_cast<size_t>(nchunks) * g->nitems * C + 1);
-    s.rowcnt = cv.take<int32_t>(static_cast<size_t>(nchunks) * g->nlong + 1);
-    s.dotcta = cv.take<double>(static_cast<size_t>(nchunks) * g->nshort * C + 1);
+// sizes for the largest of several operators (LRC reuses one scratch)
+struct SpmmDims {
+    int64_t nseg = 0, nlong = 0, ncta = 0;
+    void add(const kz_graph* g) {
+        if (!g) return;
+        nseg = std::max<int64_t>(nseg, g->nseg);
+        nlong = std::max<int64_t>(nlong, g->nlong);
+        ncta = std::max<int64_t>(ncta, g->ncta);
+    }
+};
+
+inline void carve_spmm_scratch(Carver& cv, const SpmmDims& d, int nchunks, int C, SpmmScratch& s) {
+    s.partial = cv.take<double>(static_cast<size_t>(nchunks) * d.nseg * C + 1);
+    s.rowcnt = cv.take<int32_t>(static_cast<size_t>(nchunks) * d.nlong + 1);
+    s.dotcta = cv.take<double>(static_cast<size_t>(nchunks) * d.ncta * C + 1);
     s.chunkcnt = cv.take<int32_t>(nchunks + 1);
 }
+inline void carve_spmm_scratch(Carver& cv, const kz_graph* g, int nchunks, int C, SpmmScratch& s) {
+    SpmmDims d;
+    d.add(g);
+    carve_spmm_scratch(cv, d, nchunks, C, s);
+}
 
-inline int zero_spmm_counters(const kz_graph* g, int nchunks, const SpmmScratch& s,
-                              cudaStream_t st) {
-    KZ_CUDA(cudaMemsetAsync(s.rowcnt, 0, sizeof(int32_t) * (static_cast<size_t>(nchunks) * g->nlong + 1), st));
+inline int zero_spmm_counters(const SpmmDims& d, int nchunks, const SpmmScratch& s, cudaStream_t st) {
+    KZ_CUDA(cudaMemsetAsync(s.rowcnt, 0, sizeof(int32_t) * (static_cast<size_t>(nchunks) * d.nlong + 1), st));
     KZ_CUDA(cudaMemsetAsync(s.chunkcnt, 0, sizeof(int32_t) * (nchunks + 1), st));
     return KZ_OK;
+}
+inline int zero_spmm_counters(const kz_graph* g, int nchunks, const SpmmScratch& s, cudaStream_t st) {
+    SpmmDims d;
+    d.add(g);
+    return zero_spmm_counters(d, nchunks, s, st);
 }
 
 inline SpmmArgs make_spmm_args(const kz_graph* g, const SpmmScratch& s) {
@@ -392,16 +448,12 @@ inline SpmmArgs make_spmm_args(const kz_graph* g, const SpmmScratch& s) {
     a.cols = static_cast<int32_t>(g->cols);
     a.rowptr = g->rowptr;
     a.colidx = g->colidx;
-    a.seg = g->seg;
+    a.tasks = g->tasks;
+    a.cta_task = g->cta_task;
+    a.long_seg0 = g->long_seg0;
+    a.ncta = g->ncta;
     a.nlong = g->nlong;
-    a.nitems = g->nitems;
-    a.nshort = g->nshort;
-    a.nlongcta = g->nlongcta;
-    a.long_rows = g->long_rows;
-    a.long_first = g->long_first;
-    a.item_lrow = g->item_lrow;
-    a.cta_rows = g->cta_rows;
-    a.cta_long = g->cta_long;
+    a.nseg = g->nseg;
     a.partial = s.partial;
     a.rowcnt = s.rowcnt;
     a.dotcta = s.dotcta;
@@ -409,18 +461,32 @@ inline SpmmArgs make_spmm_args(const kz_graph* g, const SpmmScratch& s) {
     return a;
 }
 
-inline int launch_spmm(const kz_graph* g, int C, int nchunks, const SpmmArgs& a,
-                       cudaStream_t st) {
-    const unsigned grid = static_cast<unsigned>(nchunks) * (g->nlongcta + g->nshort);
+inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(nchunks) * g->ncta;
+    if (grid == 0) return KZ_OK;
+    if (a.ldxg == 0) a.ldxg = g->cols * C;
+    if (a.ldxs == 0) a.ldxs = g->rows * C;
+    if (a.ldz == 0) a.ldz = g->rows * C;
+    if (a.ldy == 0) a.ldy = g->rows * C;
+    if (a.ldd == 0) a.ldd = g->rows * C;
+    a.vals = g->vals;
+    const bool w = g->vals != nullptr;
+#define KZ_SPMM_CASE(CC)                                                                  \
+    case CC:                                                                              \
+        if (w) spmm_kernel<CC, true><<<grid, kThreads, 0, st>>>(a);                        \
+        else spmm_kernel<CC, false><<<grid, kThreads, 0, st>>>(a);                         \
+        break;
     switch (C) {
-        case 1: spmm_kernel<1><<<grid, kThreads, 0, st>>>(a); ::kz::note_launch(); break;
-        case 2: spmm_kernel<2><<<grid, kThreads, 0, st>>>(a); ::kz::note_launch(); break;
-        case 4: spmm_kernel<4><<<grid, kThreads, 0, st>>>(a); ::kz::note_launch(); break;
-        case 8: spmm_kernel<8><<<grid, kThreads, 0, st>>>(a); ::kz::note_launch(); break;
-        case 16: spmm_kernel<16><<<grid, kThreads, 0, st>>>(a); ::kz::note_launch(); break;
-        case 32: spmm_kernel<32><<<grid, kThreads, 0, st>>>(a); ::kz::note_launch(); break;
+        KZ_SPMM_CASE(1)
+        KZ_SPMM_CASE(2)
+        KZ_SPMM_CASE(4)
+        KZ_SPMM_CASE(8)
+        KZ_SPMM_CASE(16)
+        KZ_SPMM_CASE(32)
         default: return fail(KZ_EARG, "unsupported chunk width");
     }
+#undef KZ_SPMM_CASE
+    note_launch();
     KZ_LAUNCH_CHECK();
     return KZ_OK;
 }

@@ -77,9 +77,10 @@ def test_spmm_matches_scipy(torch, kz, graph, b, C):
     op.spmm(Xd, Yd, b=b, chunk=C, Xs=Xd, s1=1.0, s2=-beta, dots=dots)
     Y = from_blk(Yd.cpu().numpy(), n, b, C)
     want = X - beta * (a @ X)
-    long_rows = np.diff(off) > 512
-    # short rows sum in CSR order with the same roundings as scipy: bit-exact
-    assert np.array_equal(Y[~long_rows], want[~long_rows])
+    split_rows = np.diff(off) > 32
+    # short rows (one lane group each) sum in CSR order with the same
+    # roundings as scipy: bit-exact; warp-split rows differ by roundoff only
+    assert np.array_equal(Y[~split_rows], want[~split_rows])
     assert np.abs(Y - want).max() <= 1e-13 * np.abs(want).max()
     want_dots = np.einsum("ij,ij->j", X, want)
     assert np.allclose(dots.cpu().numpy(), want_dots, rtol=1e-12, atol=0)
@@ -199,7 +200,7 @@ def test_cg_batch_at_config_sizes(torch, kz, cfg):
     scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=1e-8, device=True)
     a = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
     for j in np.linspace(0, b - 1, 6).astype(int):
-        want, orep = O.query_cg_csr(a, beta, int(qs[j]), tol=1e-8)
+        want, orep = O.query_cg_csr(a, beta, g.internal_id(int(qs[j])), tol=1e-8)
         assert abs(reps[j].iterations - orep.iterations) <= 1
         assert rel(scores[j].cpu().numpy(), want) <= REL_TOL
 
