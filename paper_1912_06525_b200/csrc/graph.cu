@@ -43,15 +43,14 @@ void free_graph(kz_graph* g) {
     cudaFree(g->colidx);
     cudaFree(g->vals);
     cudaFree(g->tasks);
-    cudaFree(g->cta_task);
+    cudaFree(g->group_first);
     cudaFree(g->long_seg0);
     delete g;
 }
 
-// Host schedule for K1 (see spmm.cuh): warp tasks in row order and
-// cost-balanced contiguous task ranges per CTA.
+// Host schedule for K1 (see spmm.cuh): warp tasks in row order.
 void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<int4>& tasks,
-                    std::vector<int32_t>& cta_task, std::vector<int32_t>& long_seg0, int32_t& max_deg) {
+                    std::vector<int32_t>& long_seg0, std::vector<int32_t>& group_first, int32_t& max_deg) {
     std::vector<double> cost;
     int64_t s_open = -1, s_rows = 0;
     double s_cost = 0.0;
@@ -94,23 +93,22 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<in
     }
     close_s(rows);
     long_seg0.push_back(nseg);
-    double total = 0.0;
-    for (double c : cost) total += c;
-    const double target = std::max(256.0, std::min(16384.0, total / (2.0 * kNumSMs)));
-    cta_task.push_back(0);
+    // warp work units: consecutive tasks up to ~kGroupCost neighbour-equivalents
+    // (at most kGroupTasks tasks); a hub segment is a unit of its own
+    group_first.push_back(0);
     double acc = 0.0;
     int cnt = 0;
     for (size_t t = 0; t < tasks.size(); ++t) {
-        if (cnt > 0 && (acc + cost[t] > target || cnt >= kTaskCap)) {
-            cta_task.push_back(static_cast<int32_t>(t));
+        if (cnt > 0 && (acc + cost[t] > kGroupCost || cnt >= kGroupTasks)) {
+            group_first.push_back(static_cast<int32_t>(t));
             acc = 0.0;
             cnt = 0;
         }
         acc += cost[t];
         ++cnt;
     }
-    if (tasks.empty() || cta_task.back() != static_cast<int32_t>(tasks.size()))
-        cta_task.push_back(static_cast<int32_t>(tasks.size()));
+    if (group_first.back() != static_cast<int32_t>(tasks.size()))
+        group_first.push_back(static_cast<int32_t>(tasks.size()));
 }
 
 }  // namespace
@@ -146,10 +144,10 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
     std::vector<int32_t> rp32(rows + 1);
     for (int64_t i = 0; i <= rows; ++i) rp32[i] = static_cast<int32_t>(rp[i]);
     std::vector<int4> tasks;
-    std::vector<int32_t> cta_task, long_seg0;
-    build_schedule(rp, rows, tasks, cta_task, long_seg0, g->max_deg);
+    std::vector<int32_t> long_seg0, group_first;
+    build_schedule(rp, rows, tasks, long_seg0, group_first, g->max_deg);
+    g->ngroups = static_cast<int32_t>(group_first.size()) - 1;
     g->ntasks = static_cast<int32_t>(tasks.size());
-    g->ncta = static_cast<int32_t>(cta_task.size()) - 1;
     g->nlong = static_cast<int32_t>(long_seg0.size()) - 1;
     g->nseg = long_seg0.back();
 
@@ -157,7 +155,7 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
     if ((st = upload(&g->rowptr, rp32.data(), rows + 1)) ||
         (st = upload(&g->colidx, static_cast<const int32_t*>(nullptr), nnz)) ||
         (st = upload(&g->tasks, tasks.data(), tasks.size())) ||
-        (st = upload(&g->cta_task, cta_task.data(), cta_task.size())) ||
+        (st = upload(&g->group_first, group_first.data(), group_first.size())) ||
         (st = upload(&g->long_seg0, long_seg0.data(), long_seg0.size())) ||
         (vals && (st = upload(&g->vals, static_cast<const double*>(nullptr), nnz)))) {
         free_graph(g);

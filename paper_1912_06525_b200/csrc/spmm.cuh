@@ -36,8 +36,10 @@
 namespace kz {
 constexpr int kMedDeg = 32;      // rows with deg <= kMedDeg are "short"
 constexpr int kSegLen = 1024;    // rows with deg > kSegLen are split into segments
-constexpr int kTaskCap = 128;    // max tasks per CTA (dot slots in shared memory)
-constexpr int kSpmmMinBlocks = 2;
+constexpr int kGroupTasks = 8;   // max tasks a warp dequeues at once (one dot slot)
+constexpr double kGroupCost = 1024.0;  // max neighbour-equivalents per work unit
+constexpr int kSuperGroups = 256; // groups reduced together by their last finisher
+constexpr int kSpmmMinBlocks = 5;
 }  // namespace kz
 
 struct kz_graph {
@@ -47,8 +49,8 @@ struct kz_graph {
     double* vals = nullptr;     // optional fp64 values (weighted operator, e.g. M11^-1)
     int32_t ntasks = 0;
     int4* tasks = nullptr;      // {a, b, type, k}: S {r0, r1}, M {row}, L {row, lidx, seg k}
-    int32_t ncta = 0;           // CTAs per chunk
-    int32_t* cta_task = nullptr;    // [ncta+1] task ranges
+    int32_t ngroups = 0;        // warp work units (consecutive task ranges)
+    int32_t* group_first = nullptr;  // [ngroups+1]
     int32_t nlong = 0;              // rows with deg > kSegLen
     int32_t nseg = 0;               // their segments
     int32_t* long_seg0 = nullptr;   // [nlong+1] first segment slot of each long row
@@ -183,9 +185,13 @@ struct SpmmArgs {
     const int32_t* __restrict__ rowptr;
     const int32_t* __restrict__ colidx;
     const int4* __restrict__ tasks;
-    const int32_t* __restrict__ cta_task;
+    const int32_t* __restrict__ group_first;
     const int32_t* __restrict__ long_seg0;
-    int32_t ncta, nlong, nseg;
+    int32_t ntasks, nlong, nseg;
+    int32_t ngroups;    // task groups (kGroupTasks consecutive tasks) per chunk
+    int32_t nsuper;     // super groups (kSuperGroups groups) per chunk
+    int32_t nchunks;
+    int32_t nwarps;     // warps of the (persistent) launch
     const double* Xg;
     const double* Xs;
     const double* Z;
@@ -197,8 +203,11 @@ struct SpmmArgs {
     double s0, s1, s2;
     double* partial;   // [nchunks][nseg][C] long-row segment sums
     int32_t* rowcnt;   // [nchunks][nlong] finished-segment counters
-    double* dotcta;    // [nchunks][ncta][C]
-    int32_t* chunkcnt; // [nchunks]
+    double* gslot;     // [nchunks][ngroups][C] group dot partials
+    double* sslot;     // [nchunks][nsuper][C] super-group dot partials
+    int32_t* scnt;     // [nchunks][nsuper] finished groups per super group
+    int32_t* ccnt;     // [nchunks] finished super groups per chunk
+    int32_t* queue;    // [2] work-queue head, exited warps
     const int32_t* chunk_active;  // optional per-chunk skip flags
     int32_t want_dot;
     DotHook hook;
@@ -243,160 +252,202 @@ __device__ __forceinline__ void apply_dot_hook(const DotHook& h, int col, double
     }
 }
 
+// Fixed-order sum over `cnt` partials of width C (stride C), one warp; lane
+// c < C returns column c.  8 independent accumulators keep loads in flight;
+// the combination order is fixed, so the result is deterministic.
+template <int C>
+__device__ __forceinline__ double warp_fixed_sum(const double* part, int cnt, int lane) {
+    constexpr int LPC = (32 / C) < 8 ? (32 / C) : 8;  // lanes per column (<= 8)
+    const int c = lane % C, sub = lane / C;
+    double s = 0.0;
+    if (sub < LPC) {
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        int q = sub;
+        for (; q + 3 * LPC < cnt; q += 4 * LPC) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] += __ldcg(part + static_cast<size_t>(q + u * LPC) * C + c);
+        }
+        for (; q < cnt; q += LPC) a[0] += __ldcg(part + static_cast<size_t>(q) * C + c);
+        s = (a[0] + a[1]) + (a[2] + a[3]);
+    }
+#pragma unroll
+    for (int off = C; off < C * LPC; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+}
+
+// Persistent, warp-granular K1.  Every warp pulls groups of kGroupTasks
+// consecutive tasks from one chunk-major queue (so the L2 working set stays
+// about one chunk), runs them, and publishes the group's dot partial into
+// its fixed slot.  The warp that completes a super group reduces its slots in
+// order; the warp that completes a chunk's last super group reduces those
+// and runs the CG/PCG hook.  No block-wide barrier anywhere.
 template <int C, bool W>
 __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs a) {
     using K = Cfg<C>;
     constexpr int VEC = K::VEC;
-    const int chunk = blockIdx.x / a.ncta;
-    const int p = blockIdx.x - chunk * a.ncta;
-    if (a.chunk_active && !a.chunk_active[chunk]) return;
-
-    __shared__ double slot[kTaskCap * C];
-    __shared__ double sm[kThreads];
-    __shared__ int next_task;
-    __shared__ int is_last;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int gw = lane / K::G, lg = lane % K::G, gbase = gw * K::G;
     const unsigned gmask = (K::G == 32) ? 0xffffffffu : (((1u << K::G) - 1u) << gbase);
-    const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.ldxg;
-    const int t0 = a.cta_task[p], nt = a.cta_task[p + 1] - t0;
-    if (threadIdx.x == 0) next_task = 0;
-    __syncthreads();
-
-    auto epilogue = [&](int row, const double (&acc)[VEC], double (&dacc)[VEC]) {
-        const size_t roff = static_cast<size_t>(row) * C + lg * VEC;
-        double y[VEC];
-        if (a.Xs) {
-            double xs[VEC];
-            ld_plain<VEC>(a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, xs);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q)
-                y[q] = __dadd_rn(__dmul_rn(a.s1, xs[q]), __dmul_rn(a.s2, acc[q]));
-        } else {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) y[q] = __dmul_rn(a.s2, acc[q]);
-        }
-        if (a.Z) {
-            double z[VEC];
-            ld_plain<VEC>(a.Z + static_cast<size_t>(chunk) * a.ldz + roff, z);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(a.s0, z[q]), y[q]);
-        }
-        st_plain<VEC>(a.Y + static_cast<size_t>(chunk) * a.ldy + roff, y);
-        if (a.want_dot) {
-            double d[VEC];
-            ld_plain<VEC>(a.D ? a.D + static_cast<size_t>(chunk) * a.ldd + roff
-                              : a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, d);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) dacc[q] = fma(d[q], y[q], dacc[q]);
-        }
-    };
-    auto warp_sum = [&](double (&v)[VEC]) {
-#pragma unroll
-        for (int off = K::G; off < 32; off <<= 1)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
-    };
+    const int total = a.ngroups * a.nchunks;
 
     while (true) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(&next_task, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= nt) break;
-        const int4 task = a.tasks[t0 + t];
+        int g = 0;
+        if (lane == 0) g = atomicAdd(a.queue, 1);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= total) break;
+        const int chunk = g / a.ngroups, gl = g - chunk * a.ngroups;
+        if (a.chunk_active && !a.chunk_active[chunk]) continue;
+        const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.ldxg;
         double dacc[VEC];
 #pragma unroll
         for (int q = 0; q < VEC; ++q) dacc[q] = 0.0;
-        if (task.z == TASK_S) {
-            for (int row = task.x + gw; row < task.y; row += K::NGW) {
+
+        auto epilogue = [&](int row, const double (&acc)[VEC]) {
+            const size_t roff = static_cast<size_t>(row) * C + lg * VEC;
+            double y[VEC];
+            if (a.Xs) {
+                double xs[VEC];
+                ld_plain<VEC>(a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, xs);
+#pragma unroll
+                for (int q = 0; q < VEC; ++q)
+                    y[q] = __dadd_rn(__dmul_rn(a.s1, xs[q]), __dmul_rn(a.s2, acc[q]));
+            } else {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) y[q] = __dmul_rn(a.s2, acc[q]);
+            }
+            if (a.Z) {
+                double z[VEC];
+                ld_plain<VEC>(a.Z + static_cast<size_t>(chunk) * a.ldz + roff, z);
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(a.s0, z[q]), y[q]);
+            }
+            st_plain<VEC>(a.Y + static_cast<size_t>(chunk) * a.ldy + roff, y);
+            if (a.want_dot) {
+                double d[VEC];
+                ld_plain<VEC>(a.D ? a.D + static_cast<size_t>(chunk) * a.ldd + roff
+                                  : a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, d);
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) dacc[q] = fma(d[q], y[q], dacc[q]);
+            }
+        };
+        auto warp_sum = [&](double (&v)[VEC]) {
+#pragma unroll
+            for (int off = K::G; off < 32; off <<= 1)
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+        };
+
+        const int t_end = a.group_first[gl + 1];
+        for (int t = a.group_first[gl]; t < t_end; ++t) {
+            const int4 task = a.tasks[t];
+            if (task.z == TASK_S) {
+                for (int row = task.x + gw; row < task.y; row += K::NGW) {
+                    double acc[VEC];
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+                    gather_rows<C, W>(a.colidx, a.rowptr[row], a.rowptr[row + 1], K::R, Xc, lg, gbase,
+                                      gmask, acc, a.vals);
+                    epilogue(row, acc);
+                }
+            } else if (task.z == TASK_M) {
+                const int row = task.x;
                 double acc[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-                gather_rows<C, W>(a.colidx, a.rowptr[row], a.rowptr[row + 1], K::R, Xc, lg, gbase,
-                                  gmask, acc, a.vals);
-                epilogue(row, acc, dacc);
-            }
-        } else if (task.z == TASK_M) {
-            const int row = task.x;
-            double acc[VEC];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-            gather_rows<C, W>(a.colidx, a.rowptr[row] + gw * K::R, a.rowptr[row + 1], K::NGW * K::R,
-                              Xc, lg, gbase, gmask, acc, a.vals);
-            warp_sum(acc);
-            if (gw == 0) epilogue(row, acc, dacc);
-        } else {
-            // long-row segment k of long row lidx
-            const int row = task.x, lidx = task.y, k = task.w;
-            const int s0 = a.long_seg0[lidx], nseg = a.long_seg0[lidx + 1] - s0;
-            const int beg = a.rowptr[row] + k * kSegLen;
-            const int end = min(beg + kSegLen, a.rowptr[row + 1]);
-            double acc[VEC];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-            gather_rows<C, W>(a.colidx, beg + gw * K::R, end, K::NGW * K::R, Xc, lg, gbase, gmask,
-                              acc, a.vals);
-            warp_sum(acc);
-            double* pbase = a.partial + static_cast<size_t>(chunk) * a.nseg * C;
-            int* cnt = a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lidx;
-            if (k < nseg - 1) {
-                if (lane < K::G) {
-                    st_plain<VEC>(pbase + static_cast<size_t>(s0 + k) * C + lg * VEC, acc);
-                    __threadfence();
-                }
-                __syncwarp();
-                if (lane == 0) atomicAdd(cnt, 1);
+                gather_rows<C, W>(a.colidx, a.rowptr[row] + gw * K::R, a.rowptr[row + 1], K::NGW * K::R,
+                                  Xc, lg, gbase, gmask, acc, a.vals);
+                warp_sum(acc);
+                if (gw == 0) epilogue(row, acc);
             } else {
-                // last segment: wait for the others, combine in segment order
-                if (lane == 0) {
-                    while (atomicAdd(cnt, 0) < nseg - 1) __nanosleep(64);
-                    __threadfence();
+                // long-row segment k of long row lidx
+                const int row = task.x, lidx = task.y, k = task.w;
+                const int s0 = a.long_seg0[lidx], nseg = a.long_seg0[lidx + 1] - s0;
+                const int beg = a.rowptr[row] + k * kSegLen;
+                const int end = min(beg + kSegLen, a.rowptr[row + 1]);
+                double acc[VEC];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+                gather_rows<C, W>(a.colidx, beg + gw * K::R, end, K::NGW * K::R, Xc, lg, gbase, gmask,
+                                  acc, a.vals);
+                warp_sum(acc);
+                double* pbase = a.partial + static_cast<size_t>(chunk) * a.nseg * C;
+                int* cnt = a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lidx;
+                if (k < nseg - 1) {
+                    if (lane < K::G) {
+                        st_plain<VEC>(pbase + static_cast<size_t>(s0 + k) * C + lg * VEC, acc);
+                        __threadfence();
+                    }
+                    __syncwarp();
+                    if (lane == 0) atomicAdd(cnt, 1);
+                } else {
+                    // last segment: the others were dequeued earlier by running
+                    // warps; wait for them and combine in segment order
+                    if (lane == 0) {
+                        while (atomicAdd(cnt, 0) < nseg - 1) __nanosleep(64);
+                        __threadfence();
+                    }
+                    __syncwarp();
+                    double tot[VEC];
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) tot[q] = 0.0;
+                    for (int s = 0; s < nseg - 1; ++s) {
+                        const double* src = pbase + static_cast<size_t>(s0 + s) * C + lg * VEC;
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) tot[q] += __ldcg(src + q);
+                    }
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) tot[q] += acc[q];
+                    if (gw == 0) epilogue(row, tot);
+                    __syncwarp();
+                    if (lane == 0) *cnt = 0;  // re-arm for the next launch
                 }
-                __syncwarp();
-                double tot[VEC];
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) tot[q] = 0.0;
-                for (int s = 0; s < nseg - 1; ++s) {
-                    const double* src = pbase + static_cast<size_t>(s0 + s) * C + lg * VEC;
-#pragma unroll
-                    for (int q = 0; q < VEC; ++q) tot[q] += __ldcg(src + q);
-                }
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) tot[q] += acc[q];
-                if (gw == 0) epilogue(row, tot, dacc);
-                __syncwarp();
-                if (lane == 0) *cnt = 0;  // re-arm for the next launch
             }
         }
-        if (a.want_dot) {
-            warp_sum(dacc);
-            if (lane < K::G) {
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) slot[t * C + lg * VEC + q] = dacc[q];
-            }
-        }
-    }
+        if (!a.want_dot) continue;
 
-    if (!a.want_dot) return;
-    __syncthreads();
-    // task slots in task order -> CTA partial -> last CTA of the chunk
-    if (threadIdx.x < C) {
-        double s = 0.0;
-        for (int t = 0; t < nt; ++t) s += slot[t * C + threadIdx.x];
-        a.dotcta[(static_cast<size_t>(chunk) * a.ncta + p) * C + threadIdx.x] = s;
+        // ---- deterministic dot reduction: group -> super group -> chunk ----
+        warp_sum(dacc);
+        double* gs = a.gslot + (static_cast<size_t>(chunk) * a.ngroups + gl) * C;
+        if (lane < K::G) {
+            st_plain<VEC>(gs + lg * VEC, dacc);
+            __threadfence();
+        }
+        __syncwarp();
+        const int sg = gl / kSuperGroups;
+        const int sg_groups = min(kSuperGroups, a.ngroups - sg * kSuperGroups);
+        int last = 0;
+        if (lane == 0)
+            last = atomicAdd(a.scnt + static_cast<size_t>(chunk) * a.nsuper + sg, 1) == sg_groups - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
         __threadfence();
+        const double sv = warp_fixed_sum<C>(a.gslot + (static_cast<size_t>(chunk) * a.ngroups + sg * kSuperGroups) * C,
+                                            sg_groups, lane);
+        if (lane < C) {
+            a.sslot[(static_cast<size_t>(chunk) * a.nsuper + sg) * C + lane] = sv;
+            __threadfence();
+        }
+        __syncwarp();
+        int clast = 0;
+        if (lane == 0) {
+            a.scnt[static_cast<size_t>(chunk) * a.nsuper + sg] = 0;
+            clast = atomicAdd(a.ccnt + chunk, 1) == a.nsuper - 1;
+        }
+        clast = __shfl_sync(0xffffffffu, clast, 0);
+        if (!clast) continue;
+        __threadfence();
+        const double v = warp_fixed_sum<C>(a.sslot + static_cast<size_t>(chunk) * a.nsuper * C, a.nsuper, lane);
+        if (lane < C) apply_dot_hook(a.hook, chunk * C + lane, v, chunk);
+        __syncwarp();
+        if (lane == 0) {
+            a.ccnt[chunk] = 0;
+            if (a.hook.mode == 1 && a.hook.chunk_xstamp) a.hook.chunk_xstamp[chunk] = a.hook.iter;
+        }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = (atomicAdd(a.chunkcnt + chunk, 1) == a.ncta - 1);
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    const double v =
-        reduce_partials<C>(a.dotcta + static_cast<size_t>(chunk) * a.ncta * C, a.ncta, sm);
-    if (threadIdx.x < C) apply_dot_hook(a.hook, chunk * C + threadIdx.x, v, chunk);
-    if (threadIdx.x == 0) {
-        a.chunkcnt[chunk] = 0;
-        if (a.hook.mode == 1 && a.hook.chunk_xstamp) a.hook.chunk_xstamp[chunk] = a.hook.iter;
+    // the last warp out re-arms the queue for the next launch
+    if (lane == 0 && atomicAdd(a.queue + 1, 1) == a.nwarps - 1) {
+        a.queue[0] = 0;
+        a.queue[1] = 0;
     }
 }
 
@@ -404,26 +455,38 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
 struct SpmmScratch {
     double* partial = nullptr;
     int32_t* rowcnt = nullptr;
-    double* dotcta = nullptr;
-    int32_t* chunkcnt = nullptr;
+    double* gslot = nullptr;
+    double* sslot = nullptr;
+    int32_t* scnt = nullptr;
+    int32_t* ccnt = nullptr;
+    int32_t* queue = nullptr;
+    int64_t nlong_cap = 0, nsuper_cap = 0;
 };
+
+inline int64_t spmm_supers(int64_t ngroups) { return (ngroups + kSuperGroups - 1) / kSuperGroups; }
 
 // sizes for the largest of several operators (LRC reuses one scratch)
 struct SpmmDims {
-    int64_t nseg = 0, nlong = 0, ncta = 0;
+    int64_t nseg = 0, nlong = 0, ngroups = 0, nsuper = 0;
     void add(const kz_graph* g) {
         if (!g) return;
         nseg = std::max<int64_t>(nseg, g->nseg);
         nlong = std::max<int64_t>(nlong, g->nlong);
-        ncta = std::max<int64_t>(ncta, g->ncta);
+        ngroups = std::max<int64_t>(ngroups, g->ngroups);
+        nsuper = std::max<int64_t>(nsuper, spmm_supers(g->ngroups));
     }
 };
 
 inline void carve_spmm_scratch(Carver& cv, const SpmmDims& d, int nchunks, int C, SpmmScratch& s) {
     s.partial = cv.take<double>(static_cast<size_t>(nchunks) * d.nseg * C + 1);
+    s.gslot = cv.take<double>(static_cast<size_t>(nchunks) * d.ngroups * C + 1);
+    s.sslot = cv.take<double>(static_cast<size_t>(nchunks) * d.nsuper * C + 1);
     s.rowcnt = cv.take<int32_t>(static_cast<size_t>(nchunks) * d.nlong + 1);
-    s.dotcta = cv.take<double>(static_cast<size_t>(nchunks) * d.ncta * C + 1);
-    s.chunkcnt = cv.take<int32_t>(nchunks + 1);
+    s.scnt = cv.take<int32_t>(static_cast<size_t>(nchunks) * d.nsuper + 1);
+    s.ccnt = cv.take<int32_t>(nchunks + 1);
+    s.queue = cv.take<int32_t>(2);
+    s.nlong_cap = d.nlong;
+    s.nsuper_cap = d.nsuper;
 }
 inline void carve_spmm_scratch(Carver& cv, const kz_graph* g, int nchunks, int C, SpmmScratch& s) {
     SpmmDims d;
@@ -431,9 +494,13 @@ inline void carve_spmm_scratch(Carver& cv, const kz_graph* g, int nchunks, int C
     carve_spmm_scratch(cv, d, nchunks, C, s);
 }
 
+// counters are re-armed by the kernels themselves; zero them once per call
 inline int zero_spmm_counters(const SpmmDims& d, int nchunks, const SpmmScratch& s, cudaStream_t st) {
-    KZ_CUDA(cudaMemsetAsync(s.rowcnt, 0, sizeof(int32_t) * (static_cast<size_t>(nchunks) * d.nlong + 1), st));
-    KZ_CUDA(cudaMemsetAsync(s.chunkcnt, 0, sizeof(int32_t) * (nchunks + 1), st));
+    const char* b0 = reinterpret_cast<const char*>(s.rowcnt);
+    const char* b1 = reinterpret_cast<const char*>(s.queue + 2);
+    KZ_CUDA(cudaMemsetAsync(s.rowcnt, 0, static_cast<size_t>(b1 - b0), st));
+    (void)d;
+    (void)nchunks;
     return KZ_OK;
 }
 inline int zero_spmm_counters(const kz_graph* g, int nchunks, const SpmmScratch& s, cudaStream_t st) {
@@ -449,21 +516,31 @@ inline SpmmArgs make_spmm_args(const kz_graph* g, const SpmmScratch& s) {
     a.rowptr = g->rowptr;
     a.colidx = g->colidx;
     a.tasks = g->tasks;
-    a.cta_task = g->cta_task;
     a.long_seg0 = g->long_seg0;
-    a.ncta = g->ncta;
+    a.ntasks = g->ntasks;
     a.nlong = g->nlong;
     a.nseg = g->nseg;
+    a.group_first = g->group_first;
+    a.ngroups = g->ngroups;
+    a.nsuper = static_cast<int32_t>(spmm_supers(g->ngroups));
     a.partial = s.partial;
     a.rowcnt = s.rowcnt;
-    a.dotcta = s.dotcta;
-    a.chunkcnt = s.chunkcnt;
+    a.gslot = s.gslot;
+    a.sslot = s.sslot;
+    a.scnt = s.scnt;
+    a.ccnt = s.ccnt;
+    a.queue = s.queue;
     return a;
 }
 
 inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaStream_t st) {
-    const unsigned grid = static_cast<unsigned>(nchunks) * g->ncta;
-    if (grid == 0) return KZ_OK;
+    const int64_t total = static_cast<int64_t>(a.ngroups) * nchunks;
+    if (total == 0) return KZ_OK;
+    // persistent grid: at most one resident wave, at most one warp per group
+    const int64_t cap = static_cast<int64_t>(kNumSMs) * kSpmmMinBlocks;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cap, (total + kWarps - 1) / kWarps)));
+    a.nchunks = nchunks;
+    a.nwarps = static_cast<int32_t>(grid) * kWarps;
     if (a.ldxg == 0) a.ldxg = g->cols * C;
     if (a.ldxs == 0) a.ldxs = g->rows * C;
     if (a.ldz == 0) a.ldz = g->rows * C;
