@@ -116,7 +116,9 @@ int kz_graph_create_weighted(int64_t rows, int64_t cols, int64_t nnz, const int6
  * K1 operators of A in partition order (full n x n, A12 n1 x n2, A21 n2 x n1,
  * A22 n2 x n2), the weighted block-diagonal M11^-1 (n1 x n1), the dense
  * row-major L^-1 and (L^-1)^T (n2 x n2), U (n2 x ell) and (U diag(d))^T
- * (ell x n2) with d = 1/(1-sigma) - 1 (factor.py:322-337).  sigma is read
+ * (ell x n2) with d = 1/(1-sigma) - 1 (factor.py:322-337).  Dense operands
+ * use a leading dimension rounded up to even (n2 + n2%2, ell + ell%2) with
+ * zero padding, so pairs of entries load as one 16-byte access.  sigma is read
  * (host) only to raise KZ_ESPECTRUM when any sigma >= 1 (factor.py:329-330). */
 typedef struct kz_lrc kz_lrc;
 typedef struct kz_lrc_desc {

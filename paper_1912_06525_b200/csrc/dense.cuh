@@ -24,13 +24,15 @@ namespace kz {
 __host__ __device__ __forceinline__ int64_t mn64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t mx64(int64_t a, int64_t b) { return a > b ? a : b; }
 
-constexpr int kDenseRows = 256;  // output rows per CTA (one per thread)
-constexpr int kDenseK = 32;      // k rows staged per step
+constexpr int kDenseThreads = 256;  // threads per CTA
+constexpr int kDenseRows = 512;     // output rows per CTA tile (<= 2 per thread)
+constexpr int kDenseK = 16;         // k rows staged per step
 constexpr int kDenseMaxCols = 64;
+constexpr int kDenseMaxSplit = 16;
 
 struct DenseArgs {
     const double* A;
-    int64_t lda, M, K;
+    int64_t lda, M, K;  // lda even, A[k*lda + i] valid (zero-padded) for i < lda
     int tri;  // 0 full, 1: only k >= i nonzero, 2: only k <= i nonzero
     const double* X;
     int64_t ldx;  // chunk stride of X (K rows)
@@ -39,67 +41,140 @@ struct DenseArgs {
     double alpha, beta;
     int ksplit;
     int64_t kper;
-    double* part;  // [mtiles][ksplit][256][NC]
+    int64_t rows_tile;  // output rows per CTA tile (256 * TM)
+    double* part;  // [mtiles][ksplit][threads][TM*NC]
     int32_t* cnt;  // [mtiles]
 };
 
 __device__ __forceinline__ bool dense_tile_empty(const DenseArgs& a, int64_t i0, int64_t k0, int64_t k1) {
     if (k0 >= k1) return true;
-    const int64_t i1 = mn64(a.M, i0 + kDenseRows) - 1;
+    const int64_t i1 = mn64(a.M, i0 + a.rows_tile) - 1;
     if (a.tri == 1 && k1 - 1 < i0) return true;  // needs some k >= i
     if (a.tri == 2 && k0 > i1) return true;      // needs some k <= i
     return false;
 }
 
-template <int C, int NCH>
-__global__ void __launch_bounds__(kDenseRows) dense_kernel(DenseArgs a) {
+// Each thread owns TM consecutive output rows and all NC columns: per k it
+// loads TM entries of A (one 16-byte load for TM = 2) and the X row from
+// shared memory in 16-byte pieces, i.e. 2*TM FMAs per shared load.
+template <int C, int NCH, int TM>
+__global__ void __launch_bounds__(kDenseThreads, (TM * C * NCH <= 16) ? 2 : 1) dense_kernel(DenseArgs a) {
     constexpr int NC = C * NCH;
+    constexpr int ROWS = kDenseThreads * TM;
+    static_assert(NC % 2 == 0 || NC == 1, "column count");
     const int mt = blockIdx.x / a.ksplit, ks = blockIdx.x - mt * a.ksplit;
-    const int64_t i0 = static_cast<int64_t>(mt) * kDenseRows;
-    const int64_t i = i0 + threadIdx.x;
+    const int64_t i0 = static_cast<int64_t>(mt) * ROWS;
+    const int64_t i = i0 + static_cast<int64_t>(threadIdx.x) * TM;
     const int64_t k0 = static_cast<int64_t>(ks) * a.kper;
     const int64_t k1 = mn64(a.K, k0 + a.kper);
-    __shared__ double xs[kDenseK][NC];
+    __shared__ __align__(16) double xs[2][kDenseK][NC];
     __shared__ int is_last;
-    double acc[NC];
+    double acc[TM][NC];
 #pragma unroll
-    for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[t][j] = 0.0;
     const bool empty = dense_tile_empty(a, i0, k0, k1);
     if (!empty) {
-        // triangular bounds for this tile
         int64_t kb = k0, ke = k1;
         if (a.tri == 1) kb = mx64(kb, i0);
-        if (a.tri == 2) ke = mn64(ke, mn64(a.M, i0 + kDenseRows));
-        kb -= (kb - k0) % kDenseK;  // keep the staging aligned to the split start
+        if (a.tri == 2) ke = mn64(ke, mn64(a.M, i0 + ROWS));
+        kb -= (kb - k0) % kDenseK;
         const bool valid = i < a.M;
-        for (int64_t kk = kb; kk < ke; kk += kDenseK) {
-            const int nk = static_cast<int>(mn64(kDenseK, ke - kk));
-            __syncthreads();
-            for (int e = threadIdx.x; e < kDenseK * NC; e += kDenseRows) {
+        constexpr int PT = (kDenseK * NC + kDenseThreads - 1) / kDenseThreads;  // staged values per thread
+        double stage[PT];
+        auto fetch = [&](int64_t kk) {
+#pragma unroll
+            for (int u = 0; u < PT; ++u) {
+                const int e = threadIdx.x + u * kDenseThreads;
                 const int r = e / NC, j = e % NC;
                 const int ch = j / C, c = j % C;
-                xs[r][j] = r < nk ? a.X[static_cast<size_t>(ch) * a.ldx + static_cast<size_t>(kk + r) * C + c] : 0.0;
+                stage[u] = (e < kDenseK * NC && kk + r < ke)
+                               ? a.X[static_cast<size_t>(ch) * a.ldx + static_cast<size_t>(kk + r) * C + c]
+                               : 0.0;
             }
-            __syncthreads();
-            if (valid) {
-                const double* Ap = a.A + static_cast<size_t>(kk) * a.lda + i;
-#pragma unroll 8
-                for (int r = 0; r < kDenseK; ++r) {
-                    const double av = r < nk ? __ldg(Ap + static_cast<size_t>(r) * a.lda) : 0.0;
+        };
+        auto commit = [&](int buf) {
 #pragma unroll
-                    for (int j = 0; j < NC; ++j) acc[j] = fma(av, xs[r][j], acc[j]);
+            for (int u = 0; u < PT; ++u) {
+                const int e = threadIdx.x + u * kDenseThreads;
+                if (e < kDenseK * NC) (&xs[buf][0][0])[e] = stage[u];
+            }
+        };
+        // A entries of a stage are loaded in one batch (kDenseK independent
+        // loads per thread) one stage ahead of their use, like X.
+        double an[kDenseK][TM];
+        auto fetch_a = [&](int64_t kk) {
+            const double* Ap = a.A + static_cast<size_t>(kk) * a.lda + i;
+            const int nk = static_cast<int>(mn64(kDenseK, ke - kk));
+#pragma unroll
+            for (int r = 0; r < kDenseK; ++r) {
+                if (valid && r < nk) {
+                    if constexpr (TM == 2) {
+                        const double2 p = __ldg(reinterpret_cast<const double2*>(Ap + static_cast<size_t>(r) * a.lda));
+                        an[r][0] = p.x;
+                        an[r][1] = p.y;
+                    } else {
+                        an[r][0] = __ldg(Ap + static_cast<size_t>(r) * a.lda);
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < TM; ++t) an[r][t] = 0.0;
                 }
+            }
+        };
+        fetch(kb);
+        commit(0);
+        fetch_a(kb);
+        __syncthreads();
+        int buf = 0;
+        for (int64_t kk = kb; kk < ke; kk += kDenseK) {
+            const int64_t kn = kk + kDenseK;
+            double ac[kDenseK][TM];
+#pragma unroll
+            for (int r = 0; r < kDenseK; ++r)
+#pragma unroll
+                for (int t = 0; t < TM; ++t) ac[r][t] = an[r][t];
+            if (kn < ke) {
+                fetch(kn);  // next stage in flight while computing this one
+                fetch_a(kn);
+            }
+#pragma unroll
+            for (int r = 0; r < kDenseK; ++r) {
+                if constexpr (NC == 1) {
+                    const double xv = xs[buf][r][0];
+#pragma unroll
+                    for (int t = 0; t < TM; ++t) acc[t][0] = fma(ac[r][t], xv, acc[t][0]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < NC; j += 2) {
+                        const double2 xv = *reinterpret_cast<const double2*>(&xs[buf][r][j]);
+#pragma unroll
+                        for (int t = 0; t < TM; ++t) {
+                            acc[t][j] = fma(ac[r][t], xv.x, acc[t][j]);
+                            acc[t][j + 1] = fma(ac[r][t], xv.y, acc[t][j + 1]);
+                        }
+                    }
+                }
+            }
+            if (kn < ke) {
+                commit(buf ^ 1);
+                __syncthreads();
+                buf ^= 1;
             }
         }
     }
-    auto store = [&](const double (&v)[NC]) {
-        if (i >= a.M) return;
+    auto store = [&](const double (&v)[TM][NC]) {
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-            const int ch = j / C, c = j % C;
-            double* yp = a.Y + static_cast<size_t>(ch) * a.ldy + static_cast<size_t>(i) * C + c;
-            const double s = a.alpha * v[j];
-            *yp = a.beta != 0.0 ? fma(a.beta, *yp, s) : s;
+        for (int t = 0; t < TM; ++t) {
+            if (i + t >= a.M) continue;
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                const int ch = j / C, c = j % C;
+                double* yp = a.Y + static_cast<size_t>(ch) * a.ldy + static_cast<size_t>(i + t) * C + c;
+                const double s = a.alpha * v[t][j];
+                *yp = a.beta != 0.0 ? fma(a.beta, *yp, s) : s;
+            }
         }
     };
     if (a.ksplit == 1) {
@@ -107,10 +182,12 @@ __global__ void __launch_bounds__(kDenseRows) dense_kernel(DenseArgs a) {
         return;
     }
     // split-K: publish partials, the last CTA of the row tile reduces in order
-    double* mine = a.part + ((static_cast<size_t>(mt) * a.ksplit + ks) * kDenseRows + threadIdx.x) * NC;
+    double* mine = a.part + ((static_cast<size_t>(mt) * a.ksplit + ks) * kDenseThreads + threadIdx.x) * (TM * NC);
     if (!empty) {
 #pragma unroll
-        for (int j = 0; j < NC; ++j) mine[j] = acc[j];
+        for (int t = 0; t < TM; ++t)
+#pragma unroll
+            for (int j = 0; j < NC; ++j) mine[t * NC + j] = acc[t][j];
     }
     __threadfence();
     __syncthreads();
@@ -118,15 +195,138 @@ __global__ void __launch_bounds__(kDenseRows) dense_kernel(DenseArgs a) {
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    double tot[NC];
+    double tot[TM][NC];
 #pragma unroll
-    for (int j = 0; j < NC; ++j) tot[j] = 0.0;
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) tot[t][j] = 0.0;
     for (int s = 0; s < a.ksplit; ++s) {
         const int64_t s0 = static_cast<int64_t>(s) * a.kper, s1 = mn64(a.K, s0 + a.kper);
         if (dense_tile_empty(a, i0, s0, s1)) continue;
-        const double* src = a.part + ((static_cast<size_t>(mt) * a.ksplit + s) * kDenseRows + threadIdx.x) * NC;
+        const double* src = a.part + ((static_cast<size_t>(mt) * a.ksplit + s) * kDenseThreads + threadIdx.x) * (TM * NC);
 #pragma unroll
-        for (int j = 0; j < NC; ++j) tot[j] += __ldcg(src + j);
+        for (int t = 0; t < TM; ++t)
+#pragma unroll
+            for (int j = 0; j < NC; ++j) tot[t][j] += __ldcg(src + t * NC + j);
+    }
+    store(tot);
+    if (threadIdx.x == 0) a.cnt[mt] = 0;
+}
+
+// ---- fp64 tensor-core (DMMA m8n8k4) variant for NC a multiple of 8 --------
+// P = A^T tiles (8 rows x 4 k) and X tiles (4 k x 8 cols) are loaded straight
+// into mma fragments from global memory (coalesced 64-byte row pieces of A,
+// 64-byte column pieces of X); each warp owns 8 output rows and all NC
+// columns, k-steps are software-pipelined kDmmaAhead deep.  No shared memory
+// operand traffic, so the kernel is HBM-bound on A.
+constexpr int kDmmaWarps = 8;
+constexpr int kDmmaRows = 8 * kDmmaWarps;  // rows per CTA tile
+constexpr int kDmmaAhead = 8;              // k-steps (of 4) in flight per warp
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int C, int NT>
+__global__ void __launch_bounds__(32 * kDmmaWarps) dense_dmma_kernel(DenseArgs a) {
+    constexpr int NC = 8 * NT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int mt = blockIdx.x / a.ksplit, ks = blockIdx.x - mt * a.ksplit;
+    const int64_t i0 = static_cast<int64_t>(mt) * kDmmaRows;
+    const int64_t iw = i0 + warp * 8;  // this warp's 8 rows
+    const int64_t k0 = static_cast<int64_t>(ks) * a.kper;
+    const int64_t k1 = mn64(a.K, k0 + a.kper);
+    __shared__ int is_last;
+    double acc[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+    const int fr = lane >> 2, fk = lane & 3;  // fragment row (A) / col (B), and k
+    const bool empty = dense_tile_empty(a, i0, k0, k1);
+    if (!empty && iw < a.M) {
+        int64_t kb = k0, ke = k1;
+        if (a.tri == 1) kb = mx64(kb, iw);
+        if (a.tri == 2) ke = mn64(ke, iw + 8);
+        kb -= (kb - k0) & 3;
+        const int64_t arow = iw + fr;  // P row = A column
+        const bool rowok = arow < a.lda;
+        // column j = n*8 + fr of the block -> chunk j / C, lane-in-chunk j % C
+        size_t xoff[NT];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const int j = n * 8 + fr;
+            xoff[n] = static_cast<size_t>(j / C) * a.ldx + (j % C);
+        }
+        const int64_t nsteps = (ke - kb + 3) >> 2;
+        double fa[kDmmaAhead], fb[kDmmaAhead][NT];
+        auto load = [&](int64_t st, int slot) {
+            const int64_t k = kb + st * 4 + fk;
+            const bool ok = st < nsteps && k < ke;
+            fa[slot] = (ok && rowok) ? __ldg(a.A + static_cast<size_t>(k) * a.lda + arow) : 0.0;
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+                fb[slot][n] = ok ? __ldg(a.X + xoff[n] + static_cast<size_t>(k) * C) : 0.0;
+        };
+#pragma unroll
+        for (int u = 0; u < kDmmaAhead; ++u) load(u, u);
+        for (int64_t st = 0; st < nsteps; st += kDmmaAhead) {
+#pragma unroll
+            for (int u = 0; u < kDmmaAhead; ++u) {
+                const double av = fa[u];
+                double bv[NT];
+#pragma unroll
+                for (int n = 0; n < NT; ++n) bv[n] = fb[u][n];
+                load(st + kDmmaAhead + u, u);  // refill this slot one round ahead
+#pragma unroll
+                for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[n][0], acc[n][1], av, bv[n]);
+            }
+        }
+    }
+    // D fragment: row fr, columns 2*fk, 2*fk+1 of each n-tile
+    auto store = [&](const double (&v)[NT][2]) {
+        const int64_t row = iw + fr;
+        if (row >= a.M) return;
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = n * 8 + 2 * fk + e;
+                double* yp = a.Y + static_cast<size_t>(j / C) * a.ldy + static_cast<size_t>(row) * C + (j % C);
+                const double s = a.alpha * v[n][e];
+                *yp = a.beta != 0.0 ? fma(a.beta, *yp, s) : s;
+            }
+    };
+    if (a.ksplit == 1) {
+        store(acc);
+        return;
+    }
+    double* mine = a.part + ((static_cast<size_t>(mt) * a.ksplit + ks) * (32 * kDmmaWarps) + threadIdx.x) * (2 * NT);
+    if (!empty) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            mine[2 * n] = acc[n][0];
+            mine[2 * n + 1] = acc[n][1];
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(a.cnt + mt, 1) == a.ksplit - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double tot[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) tot[n][0] = tot[n][1] = 0.0;
+    for (int sidx = 0; sidx < a.ksplit; ++sidx) {
+        const int64_t s0 = static_cast<int64_t>(sidx) * a.kper, s1 = mn64(a.K, s0 + a.kper);
+        if (dense_tile_empty(a, i0, s0, s1)) continue;
+        const double* src = a.part + ((static_cast<size_t>(mt) * a.ksplit + sidx) * (32 * kDmmaWarps) + threadIdx.x) * (2 * NT);
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            tot[n][0] += __ldcg(src + 2 * n);
+            tot[n][1] += __ldcg(src + 2 * n + 1);
+        }
     }
     store(tot);
     if (threadIdx.x == 0) a.cnt[mt] = 0;
@@ -139,33 +339,37 @@ struct DenseScratch {
     int64_t cnt_cap = 0;
 };
 
-inline void dense_plan(int64_t M, int64_t K, int& mtiles, int& ksplit, int64_t& kper) {
-    mtiles = static_cast<int>((M + kDenseRows - 1) / kDenseRows);
+inline void dense_plan(int64_t M, int64_t K, int& mtiles, int& ksplit, int64_t& kper,
+                       int64_t rows_tile = kDenseRows) {
+    mtiles = static_cast<int>((M + rows_tile - 1) / rows_tile);
     const int64_t kblocks = (K + kDenseK - 1) / kDenseK;
-    int64_t want = (2 * kNumSMs + mtiles - 1) / mtiles;  // ~2 CTAs per SM
-    want = std::max<int64_t>(1, std::min<int64_t>(want, kblocks));
+    int64_t want = (4 * kNumSMs + mtiles - 1) / mtiles;  // ~4 CTAs per SM
+    want = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, kblocks), kDenseMaxSplit));
     kper = ((kblocks + want - 1) / want) * kDenseK;
     ksplit = static_cast<int>((K + kper - 1) / kper);
     if (ksplit < 1) ksplit = 1;
 }
 
 inline size_t dense_part_doubles(int64_t M, int64_t K, int NC) {
-    int mtiles, ksplit;
-    int64_t kper;
-    dense_plan(M, K, mtiles, ksplit, kper);
-    return ksplit > 1 ? static_cast<size_t>(mtiles) * ksplit * kDenseRows * NC : 0;
+    size_t best = 0;
+    for (int64_t rows : {static_cast<int64_t>(kDenseThreads), static_cast<int64_t>(kDenseRows),
+                         static_cast<int64_t>(kDmmaRows)}) {
+        int mtiles, ksplit;
+        int64_t kper;
+        dense_plan(M, K, mtiles, ksplit, kper, rows);
+        if (ksplit > 1) best = std::max(best, static_cast<size_t>(mtiles) * ksplit * rows * NC);
+    }
+    return best;
 }
 
 // Y(chunks [c0, c0+nch)) = alpha * op(A) X + beta * Y, looping over groups
-// of chunks so each launch handles <= 64 columns.
+// of chunks so each launch handles <= 64 columns.  lda must be even with
+// A zero-padded up to lda columns (16-byte aligned pair loads).
 inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int tri, const double* X,
                         int64_t ldx, double* Y, int64_t ldy, double alpha, double beta, int C, int nch,
                         const DenseScratch& ds, cudaStream_t st) {
     if (M == 0) return KZ_OK;
-    int mtiles, ksplit;
-    int64_t kper;
-    dense_plan(M, K, mtiles, ksplit, kper);
-    // chunks per launch: the instantiated (C, NCH) combinations below
+    if (lda % 2 != 0 || lda < M + (M & 1)) return fail(KZ_EARG, "dense operand needs an even, padded lda");
     auto group = [&](int left) {
         if (C == 1) return left >= 16 ? 16 : left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
         if (C == 16) return std::min(left, 4);
@@ -174,7 +378,54 @@ inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int 
     };
     for (int c0 = 0, g = 0; c0 < nch; c0 += g) {
         g = group(nch - c0);
+        if ((C * g) % 8 == 0) {
+            const int nt = C * g / 8;
+            int mtiles, ksplit;
+            int64_t kper;
+            dense_plan(M, K, mtiles, ksplit, kper, kDmmaRows);
+            DenseArgs a{};
+            a.rows_tile = kDmmaRows;
+            a.A = A;
+            a.lda = lda;
+            a.M = M;
+            a.K = K;
+            a.tri = tri;
+            a.X = X + static_cast<size_t>(c0) * ldx;
+            a.ldx = ldx;
+            a.Y = Y + static_cast<size_t>(c0) * ldy;
+            a.ldy = ldy;
+            a.alpha = alpha;
+            a.beta = beta;
+            a.ksplit = ksplit;
+            a.kper = kper;
+            a.part = ds.part;
+            a.cnt = ds.cnt;
+            if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * kDmmaRows * g * C > ds.part_cap ||
+                               mtiles > ds.cnt_cap))
+                return fail(KZ_EARG, "dense scratch too small");
+            const unsigned grid = static_cast<unsigned>(mtiles) * ksplit;
+#define KZ_DMMA(CC, NN) dense_dmma_kernel<CC, NN><<<grid, 32 * kDmmaWarps, 0, st>>>(a)
+            if (C == 8 && nt == 1) KZ_DMMA(8, 1);
+            else if (C == 16 && nt == 2) KZ_DMMA(16, 2);
+            else if (C == 16 && nt == 4) KZ_DMMA(16, 4);
+            else if (C == 16 && nt == 6) KZ_DMMA(16, 6);
+            else if (C == 16 && nt == 8) KZ_DMMA(16, 8);
+            else if (C == 32 && nt == 4) KZ_DMMA(32, 4);
+            else if (C == 32 && nt == 8) KZ_DMMA(32, 8);
+            else if (C == 1 && nt == 1) KZ_DMMA(1, 1);
+            else if (C == 1 && nt == 2) KZ_DMMA(1, 2);
+            else return fail(KZ_EARG, "dmma: unsupported column group");
+#undef KZ_DMMA
+            note_launch();
+            KZ_LAUNCH_CHECK();
+            continue;
+        }
+        const int tm = 1;  // TM = 2 spills under the 2-CTA register budget
+        int mtiles, ksplit;
+        int64_t kper;
+        dense_plan(M, K, mtiles, ksplit, kper, static_cast<int64_t>(kDenseThreads) * tm);
         DenseArgs a{};
+        a.rows_tile = static_cast<int64_t>(kDenseThreads) * tm;
         a.A = A;
         a.lda = lda;
         a.M = M;
@@ -190,27 +441,26 @@ inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int 
         a.kper = kper;
         a.part = ds.part;
         a.cnt = ds.cnt;
-        if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * kDenseRows * g * C > ds.part_cap ||
+        if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * a.rows_tile * g * C > ds.part_cap ||
                            mtiles > ds.cnt_cap))
             return fail(KZ_EARG, "dense scratch too small");
         const unsigned grid = static_cast<unsigned>(mtiles) * ksplit;
-        // NC = C*g must be one of the instantiated widths
         const int nc = C * g;
-#define KZ_DENSE(CC, NN) dense_kernel<CC, NN><<<grid, kDenseRows, 0, st>>>(a)
-        if (C == 1 && g == 1) KZ_DENSE(1, 1);
-        else if (C == 1 && g == 2) KZ_DENSE(1, 2);
-        else if (C == 1 && g == 4) KZ_DENSE(1, 4);
-        else if (C == 1 && g == 8) KZ_DENSE(1, 8);
-        else if (C == 1 && g == 16) KZ_DENSE(1, 16);
-        else if (C == 2 && g == 1) KZ_DENSE(2, 1);
-        else if (C == 4 && g == 1) KZ_DENSE(4, 1);
-        else if (C == 8 && g == 1) KZ_DENSE(8, 1);
-        else if (C == 16 && g == 1) KZ_DENSE(16, 1);
-        else if (C == 16 && g == 2) KZ_DENSE(16, 2);
-        else if (C == 16 && g == 3) KZ_DENSE(16, 3);
-        else if (C == 16 && g == 4) KZ_DENSE(16, 4);
-        else if (C == 32 && g == 1) KZ_DENSE(32, 1);
-        else if (C == 32 && g == 2) KZ_DENSE(32, 2);
+#define KZ_DENSE(CC, NN, TT) dense_kernel<CC, NN, TT><<<grid, kDenseThreads, 0, st>>>(a)
+        if (C == 1 && g == 1) KZ_DENSE(1, 1, 1);
+        else if (C == 1 && g == 2) KZ_DENSE(1, 2, 1);
+        else if (C == 1 && g == 4) KZ_DENSE(1, 4, 1);
+        else if (C == 1 && g == 8) KZ_DENSE(1, 8, 1);
+        else if (C == 1 && g == 16) KZ_DENSE(1, 16, 1);
+        else if (C == 2 && g == 1) KZ_DENSE(2, 1, 1);
+        else if (C == 4 && g == 1) KZ_DENSE(4, 1, 1);
+        else if (C == 8 && g == 1) KZ_DENSE(8, 1, 1);
+        else if (C == 16 && g == 1) KZ_DENSE(16, 1, 1);
+        else if (C == 16 && g == 2) KZ_DENSE(16, 2, 1);
+        else if (C == 16 && g == 3) KZ_DENSE(16, 3, 1);
+        else if (C == 16 && g == 4) KZ_DENSE(16, 4, 1);
+        else if (C == 32 && g == 1) KZ_DENSE(32, 1, 1);
+        else if (C == 32 && g == 2) KZ_DENSE(32, 2, 1);
         else return fail(KZ_EARG, "dense: unsupported column group " + std::to_string(nc));
 #undef KZ_DENSE
         note_launch();

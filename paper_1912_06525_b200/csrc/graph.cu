@@ -63,11 +63,16 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<in
     };
     int32_t nlong = 0, nseg = 0;
     max_deg = 0;
+    // granularity: aim for >= ~2 work units per resident warp of one chunk pass
+    const double est_total = static_cast<double>(rp[rows]) + 4.0 * static_cast<double>(rows);
+    const double unit = std::max(64.0, std::min(kGroupCost, est_total / (2.0 * kNumSMs * kSpmmMinBlocks * kWarps)));
+    const int s_rows_max = unit >= 512.0 ? 32 : (unit >= 128.0 ? 8 : 4);
+    const double s_cost_max = std::min(256.0, unit);
     for (int64_t i = 0; i < rows; ++i) {
         const int64_t d = rp[i + 1] - rp[i];
         max_deg = std::max<int32_t>(max_deg, static_cast<int32_t>(d));
         if (d <= kMedDeg) {
-            if (s_open >= 0 && (s_rows >= 32 || s_cost + d + 4 > 256.0)) close_s(i);
+            if (s_open >= 0 && (s_rows >= s_rows_max || s_cost + d + 4 > s_cost_max)) close_s(i);
             if (s_open < 0) {
                 s_open = i;
                 s_rows = 0;
@@ -99,7 +104,7 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<in
     double acc = 0.0;
     int cnt = 0;
     for (size_t t = 0; t < tasks.size(); ++t) {
-        if (cnt > 0 && (acc + cost[t] > kGroupCost || cnt >= kGroupTasks)) {
+        if (cnt > 0 && (acc + cost[t] > unit || cnt >= kGroupTasks)) {
             group_first.push_back(static_cast<int32_t>(t));
             acc = 0.0;
             cnt = 0;

@@ -37,10 +37,11 @@ struct kz_lrc {
     const kz_graph* a21 = nullptr;
     const kz_graph* a22 = nullptr;
     const kz_graph* minv = nullptr;
-    const double* linv = nullptr;   // n2 x n2 row-major, lower triangular
-    const double* linvT = nullptr;  // n2 x n2 row-major, (L^-1)^T
-    const double* u = nullptr;      // n2 x ell row-major
-    const double* udT = nullptr;    // ell x n2 row-major, (U diag(d))^T
+    const double* linv = nullptr;   // n2 x ld2 row-major, lower triangular
+    const double* linvT = nullptr;  // n2 x ld2 row-major, (L^-1)^T
+    const double* u = nullptr;      // n2 x ldl row-major
+    const double* udT = nullptr;    // ell x ld2 row-major, (U diag(d))^T
+    int64_t ld2 = 0, ldl = 0;       // leading dimensions, rounded up to even (zero padded)
 };
 
 namespace {
@@ -97,7 +98,7 @@ void carve_lrc(Carver& cv, const kz_lrc* h, int b, int C, LrcWork& w) {
     dp = std::max(dp, dense_part_doubles(n2, ell, NC));
     w.ds.part = cv.take<double>(dp + 1);
     w.ds.part_cap = dp;
-    w.ds.cnt_cap = (n2 + kDenseRows - 1) / kDenseRows + 1;
+    w.ds.cnt_cap = (std::max(n2, ell) + kDmmaRows - 1) / kDmmaRows + 1;
     w.ds.cnt = cv.take<int32_t>(w.ds.cnt_cap);
     SolveState& s = w.st;
     s.rs = cv.take<double>(w.bpad);
@@ -230,17 +231,17 @@ struct LrcCtx {
     int precond(const double* r, int64_t ldr, double* z, int64_t ldz) {
         const int64_t n2 = h->n2, ell = h->ell;
         int rc;
-        if ((rc = launch_dense(h->linvT, n2, n2, n2, 2, r, ldr, w->t2, n2 * C, 1.0, 0.0, C, nch, w->ds, st)))
+        if ((rc = launch_dense(h->linvT, h->ld2, n2, n2, 2, r, ldr, w->t2, n2 * C, 1.0, 0.0, C, nch, w->ds, st)))
             return rc;
         if (ell > 0) {
-            if ((rc = launch_dense(h->u, ell, ell, n2, 0, w->t2, n2 * C, w->cl, ell * C, 1.0, 0.0, C, nch, w->ds,
+            if ((rc = launch_dense(h->u, h->ldl, ell, n2, 0, w->t2, n2 * C, w->cl, ell * C, 1.0, 0.0, C, nch, w->ds,
                                    st)))
                 return rc;
-            if ((rc = launch_dense(h->udT, n2, n2, ell, 0, w->cl, ell * C, w->t2, n2 * C, 1.0, 1.0, C, nch,
+            if ((rc = launch_dense(h->udT, h->ld2, n2, ell, 0, w->cl, ell * C, w->t2, n2 * C, 1.0, 1.0, C, nch,
                                    w->ds, st)))
                 return rc;
         }
-        return launch_dense(h->linv, n2, n2, n2, 1, w->t2, n2 * C, z, ldz, 1.0, 0.0, C, nch, w->ds, st);
+        return launch_dense(h->linv, h->ld2, n2, n2, 1, w->t2, n2 * C, z, ldz, 1.0, 0.0, C, nch, w->ds, st);
     }
 
     int coldot(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int mode,
@@ -282,6 +283,8 @@ extern "C" int kz_lrc_create(const kz_lrc_desc* d, kz_lrc** out) {
     h->linvT = d->linvT;
     h->u = d->u;
     h->udT = d->udT;
+    h->ld2 = d->n2 + (d->n2 & 1);
+    h->ldl = d->ell + (d->ell & 1);
     *out = h;
     return KZ_OK;
 }

@@ -98,7 +98,15 @@ class DeviceLRC:
             _lib.check(lib.kz_graph_create_weighted(n1, n1, int(o[-1]), o.ctypes.data, c.ctypes.data,
                                                     v.ctypes.data, ctypes.byref(h)))
             self.minv = _Handle(lib, h)
-        dev = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+        def dev(a):
+            # row-major with the leading dimension rounded up to even, zero
+            # padded (the kernels load entry pairs as one 16-byte access)
+            a = np.asarray(a, dtype=np.float64)
+            rows, cols = a.shape
+            out = np.zeros((rows, cols + (cols & 1)))
+            out[:, :cols] = a
+            return torch.as_tensor(out).cuda()
+
         self.t_linv = self.t_linvT = self.t_u = self.t_udT = None
         sigma = np.ascontiguousarray(idx.lr.values[:ell], dtype=np.float64)
         if n2 > 0:
