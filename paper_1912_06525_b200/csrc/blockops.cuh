@@ -371,6 +371,48 @@ __global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __
     }
 }
 
+// Inverse of the output permutation: iperm[perm[i]] = i.
+static __global__ void invert_perm_kernel(const int64_t* __restrict__ perm, int64_t* __restrict__ iperm, int64_t n) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        iperm[perm[i]] = i;
+}
+
+// chunked block (solve order) -> column-major scores [b][rows] in internal
+// order, as a gather: output tile rows k..k+63 read their solve rows
+// iperm[k] (one 8*C-byte line each) and write each column coalesced.  Same
+// values as store_colmajor_kernel with perm, without the scattered stores.
+template <int C>
+__global__ void store_gather_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                    int64_t rows, int64_t ld, int b, int nchunks,
+                                    const int64_t* __restrict__ iperm, int clamp) {
+    constexpr int TR = 64;
+    __shared__ double sm[TR * (C + 1)];
+    const int64_t ntiles = (rows + TR - 1) / TR;
+    for (int64_t t = blockIdx.x; t < ntiles * nchunks; t += gridDim.x) {
+        const int chunk = static_cast<int>(t / ntiles);
+        const int64_t r0 = (t - static_cast<int64_t>(chunk) * ntiles) * TR;
+        for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
+            const int rr = e / C, c = e % C;
+            const int64_t row = r0 + rr;
+            sm[rr * (C + 1) + c] =
+                row < rows ? src[static_cast<size_t>(chunk) * ld + static_cast<size_t>(iperm[row]) * C + c] : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
+            const int c = e / TR, rr = e % TR;
+            const int col = chunk * C + c;
+            const int64_t row = r0 + rr;
+            if (col < b && row < rows) {
+                double v = sm[rr * (C + 1) + c];
+                if (clamp) v = v > 0.0 ? v : 0.0;
+                dst[static_cast<size_t>(col) * rows + row] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 template <int C>
 __global__ void broadcast_kernel(double* __restrict__ dst, const double* __restrict__ v,
                                  int64_t rows, int64_t ld, int b, int nchunks) {

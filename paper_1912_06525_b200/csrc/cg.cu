@@ -29,6 +29,7 @@ struct CgWork {
     RedScratch red;
     SolveState st;
     int64_t* qpos;
+    int64_t* iperm;  // inverse output permutation (gather-based store)
 };
 
 void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w) {
@@ -64,6 +65,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w) {
     s.n_active = cv.take<int32_t>(1);
     s.err = cv.take<int32_t>(1);
     w.qpos = cv.take<int64_t>(w.bpad);
+    w.iperm = cv.take<int64_t>(g->rows);
 }
 
 
@@ -192,7 +194,13 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
     int rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
     if (rc) return rc;
 
-    KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, a->perm, a->clamp); ::kz::note_launch());
+    if (a->perm) {
+        invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
+        ::kz::note_launch();
+        KZ_DISPATCH_C(C, store_gather_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, w.iperm, a->clamp); ::kz::note_launch());
+    } else {
+        KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, nullptr, a->clamp); ::kz::note_launch());
+    }
     KZ_LAUNCH_CHECK();
     if (a->device_ms) {
         KZ_CUDA(cudaEventRecord(e1, st));

@@ -59,6 +59,7 @@ struct LrcWork {
     SolveState st;
     double *rhs2, *resid2;
     int64_t* qpos;
+    int64_t* iperm;  // inverse output permutation (gather-based store)
 };
 
 int64_t rows_or_one(int64_t r) { return r > 0 ? r : 1; }
@@ -120,6 +121,7 @@ void carve_lrc(Carver& cv, const kz_lrc* h, int b, int C, LrcWork& w) {
     s.n_active = cv.take<int32_t>(1);
     s.err = cv.take<int32_t>(1);
     w.qpos = cv.take<int64_t>(w.bpad);
+    w.iperm = cv.take<int64_t>(n);
 }
 
 // LRC init finalize (solver.py:171-177 + 127-133): thresh = tol_eff*||f||
@@ -464,9 +466,17 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
                           nullptr, nullptr)))
             return rc;
         if ((rc = cx.coldot(w.rhs, ln, w.rhs, ln, n, FIN_WRITE, w.resid2, 0))) return rc;
-        KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tg, kThreads, 0, st>>>(a->out, w.kk, n, ln, b, nch, a->perm,
-                                                                             a->clamp);
-                      note_launch());
+        if (a->perm) {
+            invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
+            note_launch();
+            KZ_DISPATCH_C(C, store_gather_kernel<CC><<<tg, kThreads, 0, st>>>(a->out, w.kk, n, ln, b, nch, w.iperm,
+                                                                              a->clamp);
+                          note_launch());
+        } else {
+            KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tg, kThreads, 0, st>>>(a->out, w.kk, n, ln, b, nch, nullptr,
+                                                                                 a->clamp);
+                          note_launch());
+        }
     } else {
         KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tg, kThreads, 0, st>>>(a->out, w.xs, n2, l2, b, nch, nullptr,
                                                                              0);

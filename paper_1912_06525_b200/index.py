@@ -269,36 +269,82 @@ class GraphIndex(_DeviceGraphMixin):
     Used where the reference's LRC build is infeasible; the
     solver is the reference's ``cg`` (solver.py:62-101) on v - alpha*A v
     with rhs alpha*A e_q, i.e. query_cg_baseline in natural order.
+
+    ``reorder`` relabels the nodes *inside the solve* for gather locality
+    (reverse Cuthill-McKee; "auto" = only for operators above 10^6 stored
+    entries).  It is invisible at the API: right-hand sides, start vectors
+    and scores stay in internal order (the output kernel scatters back); only
+    summation order, i.e. roundoff, changes.
     """
 
     graph: Graph
     alpha: float
     spectral_norm: float = float("nan")
+    reorder: str = "auto"
 
     solver_kind = "cg"
 
     def __post_init__(self):
         self.id_map = self.graph.original_ids
+        g = self.graph
+        mode = self.reorder
+        if mode == "auto":
+            mode = "rcm" if g.nnz > 1_000_000 else None
+        self._order = None
+        if mode == "rcm":
+            self._order = rcm_order(g)
+        elif mode == "degree":
+            self._order = np.argsort(-np.diff(g.row_offsets), kind="stable")
+        elif mode not in (None, "none"):
+            raise ValueError(f"unknown reorder mode {mode!r}")
+        if self._order is not None:
+            self._inv = np.empty(g.n, dtype=np.int64)
+            self._inv[self._order] = np.arange(g.n)
 
     @property
     def n(self):
         return self.graph.n
 
     def operator(self):
+        """Device operator in the solve order."""
         cache = self._op_cache()
         if "op" not in cache:
             g = self.graph
-            cache["op"] = DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
+            if self._order is None:
+                cache["op"] = DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
+            else:
+                off, col = permute_csr(g.row_offsets, g.col_indices, self._order, self._inv)
+                cache["op"] = DeviceOperator(off, col, g.n)
         return cache["op"]
 
     def mask_operator(self):
-        return self.operator()
+        """Device operator in internal order (neighbour masks for top-k)."""
+        if self._order is None:
+            return self.operator()
+        cache = self._op_cache()
+        if "mask" not in cache:
+            g = self.graph
+            cache["mask"] = DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
+        return cache["mask"]
 
     def solve_positions(self, internal):
-        return np.asarray(internal, dtype=np.int64)
+        internal = np.asarray(internal, dtype=np.int64)
+        return internal if self._order is None else self._inv[internal]
+
+    def start_vector_to_solve(self, x0):
+        """A start vector given in internal order, in the solve order."""
+        return x0 if self._order is None else x0[self._order]
 
     def device_perm(self):
-        return None
+        if self._order is None:
+            return None
+        cache = self._op_cache()
+        if "perm" not in cache:
+            from . import _lib
+
+            torch = _lib.torch_cuda()
+            cache["perm"] = torch.as_tensor(self._order, dtype=torch.int64).cuda()
+        return cache["perm"]
 
     def adjacency_internal(self):
         return self.graph.row_offsets, self.graph.col_indices
@@ -308,6 +354,24 @@ class GraphIndex(_DeviceGraphMixin):
         out = np.zeros(g.n)
         out[g.neighbors(pos)] = self.alpha
         return out
+
+
+def rcm_order(g):
+    """Reverse Cuthill-McKee node order (locality of the K1 gathers)."""
+    import scipy.sparse.csgraph as csgraph
+
+    a = sp.csr_matrix((np.ones(g.nnz, dtype=np.int8), g.col_indices, g.row_offsets), shape=(g.n, g.n))
+    return np.asarray(csgraph.reverse_cuthill_mckee(a, symmetric_mode=True), dtype=np.int64)
+
+
+def permute_csr(offsets, cols, order, inv):
+    """Rows/cols relabelled: new row i = old row order[i], new col = inv[old col].
+    Column order within a row is kept (K1 does not need sorted rows)."""
+    deg = np.diff(offsets)[order]
+    new_off = np.zeros(order.size + 1, dtype=np.int64)
+    np.cumsum(deg, out=new_off[1:])
+    src = np.repeat(offsets[order] - new_off[:-1], deg) + np.arange(new_off[-1], dtype=np.int64)
+    return new_off, inv[cols[src]].astype(np.int32)
 
 
 # ---------------------------------------------------------------------------

@@ -91,7 +91,12 @@ def cg_solve_device(idx, positions, tol=1e-8, max_iter=None, start_seed=None, rh
         out = torch.empty((b, n), dtype=torch.float64, device="cuda")
     x0 = None
     if start_seed is not None:
-        x0 = torch.as_tensor(_start_vector(n, start_seed), dtype=torch.float64).cuda()
+        xs = _start_vector(n, start_seed)
+        # the seeded vector lives in the reference's solve space: partition
+        # order for a KLRC index, internal order for a GraphIndex
+        if hasattr(idx, "start_vector_to_solve"):
+            xs = idx.start_vector_to_solve(xs)
+        x0 = torch.as_tensor(xs, dtype=torch.float64).cuda()
     dperm = idx.device_perm() if perm else None
     reports = (_lib.KzReport * b)()
     total_ms = 0.0

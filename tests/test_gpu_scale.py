@@ -35,7 +35,7 @@ def _true_residual(kz, idx, qs, scores_t):
 
     g = idx.graph
     n, b = g.n, scores_t.shape[0]
-    op = idx.operator()
+    op = idx.mask_operator()  # internal order, like the scores
     x = scores_t.contiguous()
     mx = torch.empty_like(x)
     op.spmm(x.reshape(-1), mx.reshape(-1), b=b, chunk=1, Xs=x.reshape(-1), s1=1.0, s2=-idx.alpha)
