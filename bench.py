@@ -234,7 +234,7 @@ def main():
     d2h = b * k * 16 + b * 4 + b * 32 + 8 * int(np.max(iters_all) + 2)
 
     # ---- roofline of the dominant kernel: the K1 SpMM of one CG iteration ----
-    C = 16 if b >= 16 else 1
+    C = 32 if b >= 32 else (16 if b >= 16 else 1)  # = default_chunk(b) of the library
     nch = (b + C - 1) // C
     X = torch.randn(nch * C * n, dtype=torch.float64, device="cuda")
     Y = torch.empty_like(X)

@@ -66,8 +66,11 @@ struct Cfg {
     static constexpr int VEC = (C >= 2) ? 2 : 1;  // doubles per lane (16-byte loads)
     static constexpr int G = C / VEC;             // lanes per row group
     static constexpr int NGW = 32 / G;            // row groups per warp
-    static constexpr int R = (G >= 4) ? G : 4;    // neighbours gathered per round
-    static constexpr int PER = R / G;             // column indices loaded per lane per round
+    // neighbours gathered per round: 8 (4 for narrow groups) -- R*VEC doubles
+    // of gather registers per lane
+    static constexpr int R = (G >= 8) ? 8 : (G >= 4 ? G : 4);
+    static constexpr int PER = (R >= G) ? R / G : 1;  // indices loaded per lane per round
+    static constexpr bool PART = R < G;               // only lanes lg < R load indices
 };
 
 template <int VEC>
@@ -120,8 +123,9 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
 #pragma unroll
     for (int m = 0; m < K::PER; ++m) {
         const int pos = beg + lg + K::G * m;
-        nidx[m] = (pos < end) ? __ldg(col + pos) : 0;
-        if constexpr (W) nwv[m] = (pos < end) ? __ldg(vals + pos) : 0.0;
+        const bool ok = pos < end && (!K::PART || lg < K::R);
+        nidx[m] = ok ? __ldg(col + pos) : 0;
+        if constexpr (W) nwv[m] = ok ? __ldg(vals + pos) : 0.0;
     }
     const double* __restrict__ Xl = Xc + lg * K::VEC;
 #pragma unroll 1
@@ -131,8 +135,9 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
             idx[m] = nidx[m];
             if constexpr (W) wv[m] = nwv[m];
             const int pos = base + stride + lg + K::G * m;
-            nidx[m] = (pos < end) ? __ldg(col + pos) : 0;
-            if constexpr (W) nwv[m] = (pos < end) ? __ldg(vals + pos) : 0.0;
+            const bool ok = pos < end && (!K::PART || lg < K::R);
+            nidx[m] = ok ? __ldg(col + pos) : 0;
+            if constexpr (W) nwv[m] = ok ? __ldg(vals + pos) : 0.0;
         }
         double v[K::R][K::VEC];
         double w[K::R];
