@@ -445,6 +445,7 @@ inline int stream_ctas_per_chunk(int64_t rows, int C, int nchunks) {
         case 8: { constexpr int CC = 8; __VA_ARGS__; } break;  \
         case 16: { constexpr int CC = 16; __VA_ARGS__; } break; \
         case 32: { constexpr int CC = 32; __VA_ARGS__; } break; \
+        case 64: { constexpr int CC = 64; __VA_ARGS__; } break; \
         default: return fail(KZ_EARG, "unsupported chunk width"); \
     }
 

@@ -57,7 +57,7 @@ __host__ __device__ inline size_t blk_index(int64_t rows, int C, int64_t i, int 
 }
 
 // Supported chunk widths (columns per chunk) and the default choice for b.
-inline bool chunk_ok(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32; }
+inline bool chunk_ok(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32 || C == 64; }
 inline int default_chunk(int b) {
     if (b >= 32) return 32;  // 256-byte gathered segments, half the index passes of C=16
     if (b >= 16) return 16;

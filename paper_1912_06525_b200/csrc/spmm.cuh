@@ -565,6 +565,7 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
         KZ_SPMM_CASE(8)
         KZ_SPMM_CASE(16)
         KZ_SPMM_CASE(32)
+        KZ_SPMM_CASE(64)
         default: return fail(KZ_EARG, "unsupported chunk width");
     }
 #undef KZ_SPMM_CASE
