@@ -48,6 +48,14 @@ void free_graph(kz_graph* g) {
     delete g;
 }
 
+__global__ void check_cols_kernel(const int32_t* __restrict__ col, int64_t nnz, int32_t cols, int32_t* bad) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nnz;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t c = col[i];
+        if (c < 0 || c >= cols) atomicExch(bad, 1);
+    }
+}
+
 // Host schedule for K1 (see spmm.cuh): warp tasks in row order.
 void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<int4>& tasks,
                     std::vector<int32_t>& long_seg0, std::vector<int32_t>& group_first, int32_t& max_deg) {
@@ -172,6 +180,24 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
         if (e != cudaSuccess) {
             free_graph(g);
             return fail(KZ_ECUDA, std::string("CSR copy: ") + cudaGetErrorString(e));
+        }
+        // every column index must address a row of Xg: checked once on the
+        // device so a bad operator fails here, not as an illegal access later
+        int32_t* bad = nullptr;
+        if (cudaMalloc(&bad, sizeof(int32_t)) != cudaSuccess) {
+            free_graph(g);
+            return fail(KZ_EOOM, "validation flag");
+        }
+        cudaMemset(bad, 0, sizeof(int32_t));
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (nnz + 255) / 256));
+        check_cols_kernel<<<grid, 256>>>(g->colidx, nnz, static_cast<int32_t>(cols), bad);
+        note_launch();
+        int32_t h = 0;
+        e = cudaMemcpy(&h, bad, sizeof(int32_t), cudaMemcpyDeviceToHost);
+        cudaFree(bad);
+        if (e != cudaSuccess || h) {
+            free_graph(g);
+            return fail(e != cudaSuccess ? KZ_ECUDA : KZ_EARG, "column index out of range [0, cols)");
         }
     }
     *out = g;

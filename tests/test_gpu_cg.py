@@ -255,3 +255,11 @@ def test_katz_rank_graph_index_matches_oracle(torch, kz):
         got = preds[j].candidates
         assert [c for c, _ in got] == [c for c, _ in want]
         assert np.allclose([v for _, v in got], [v for _, v in want], rtol=1e-9, atol=0)
+
+
+def test_operator_rejects_out_of_range_columns(torch, kz):
+    off = np.array([0, 1, 2], dtype=np.int64)
+    with pytest.raises(ValueError):
+        kz.DeviceOperator(off, np.array([1, 2], dtype=np.int32), 2)  # column 2 of a 2-column operator
+    with pytest.raises(ValueError):
+        kz.DeviceOperator(off, np.array([1, -1], dtype=np.int32), 2)
