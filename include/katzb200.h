@@ -208,6 +208,13 @@ int kz_pearson_rerank(const double* profiles, const double* ref, const int64_t* 
                       const double* top_scores, const int32_t* counts, int32_t b, int32_t T1,
                       int32_t s, double* corr_out, int64_t* order_out, void* stream);
 
+/* ---- ingestion: connected components (largest_connected_component) -------
+ * labels[i] = smallest node id of i's component (the order in which the
+ * reference's BFS numbers components, graph.py:211-229), from device edge
+ * endpoints src/dst (int32[nnz], any orientation, duplicates allowed). */
+int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const int32_t* dst,
+                            int32_t* labels, void* stream);
+
 /* ---- vector helpers used by the generic cg() / lrc_pcg() drivers -------- */
 /* out[j] = sum_i X[i,j]*Y[i,j] over b columns of length n (column-major). */
 int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out, void* stream);

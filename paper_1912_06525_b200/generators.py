@@ -51,61 +51,19 @@ def rmat_graph(scale, edge_factor=16, abcd=RMAT_ABCD, seed=0):
 
 
 def rmat_graph_fast(scale, edge_factor=16, abcd=RMAT_ABCD, seed=0):
-    """rmat_graph with the dedupe/sort and the LCC relabel done by torch on
-    the GPU (ingestion plumbing; identical CSR to rmat_graph)."""
+    """rmat_graph with from_edges and the largest component on the GPU
+    (graph.from_edges_device / largest_connected_component_device); the same
+    CSR as rmat_graph."""
     import torch
 
     if not torch.cuda.is_available():
         return rmat_graph(scale, edge_factor, abcd, seed)
-    import scipy.sparse as sp
-    import scipy.sparse.csgraph as csgraph
+    from .graph import from_edges_device, largest_connected_component_device
 
     u, v, n = rmat_pairs(scale, edge_factor, abcd, seed)
-    dev = "cuda"
-    ut = torch.from_numpy(u).to(dev)
-    vt = torch.from_numpy(v).to(dev)
+    g, dev = from_edges_device(u, v, n)
     del u, v
-    keep = ut != vt
-    lo = torch.minimum(ut, vt)[keep]
-    hi = torch.maximum(ut, vt)[keep]
-    del ut, vt, keep
-    und = torch.unique(lo * n + hi)
-    del lo, hi
-    lo, hi = und // n, und % n
-    del und
-    keys = torch.cat([lo * n + hi, hi * n + lo])
-    del lo, hi
-    keys, _ = torch.sort(keys)
-    src = keys // n
-    dst = keys % n
-    del keys
-    counts = torch.bincount(src, minlength=n)
-    del src
-    # largest component on the host (scipy), same rule as largest_connected_component
-    offsets = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(counts.cpu().numpy(), out=offsets[1:])
-    dst32 = dst.to(torch.int32).cpu().numpy()
-    a = sp.csr_matrix((np.ones(dst32.size, dtype=np.int8), dst32, offsets), shape=(n, n))
-    count, labels = csgraph.connected_components(a, directed=False)
-    del a
-    sizes = np.bincount(labels, minlength=count)
-    first = np.full(count, n, dtype=np.int64)
-    np.minimum.at(first, labels, np.arange(n))
-    cands = np.flatnonzero(sizes == sizes.max())
-    best = cands[np.argmin(first[cands])]
-    keep = np.flatnonzero(labels == best)
-    lab = torch.from_numpy(labels).to(dev)
-    remap = torch.full((n,), -1, dtype=torch.int64, device=dev)
-    keep_t = torch.from_numpy(keep).to(dev)
-    remap[keep_t] = torch.arange(keep.size, device=dev)
-    row_of = torch.repeat_interleave(torch.arange(n, device=dev), counts)
-    mask = lab[row_of] == int(best)
-    del row_of
-    cols = remap[dst[mask]].cpu().numpy()
-    deg = counts[keep_t].cpu().numpy()
-    off2 = np.zeros(keep.size + 1, dtype=np.int64)
-    np.cumsum(deg, out=off2[1:])
-    return Graph(n=int(keep.size), row_offsets=off2, col_indices=cols, original_ids=keep.astype(np.int64))
+    return largest_connected_component_device(g, dev)
 
 
 def chung_lu_graph(n=10_000, gamma=2.5, mean_degree=10.0, seed=0):

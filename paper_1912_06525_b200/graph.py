@@ -156,6 +156,75 @@ def largest_connected_component(g):
                  original_ids=g.original_ids[keep].copy())
 
 
+def from_edges_device(u, v, n, original_ids=None):
+    """from_edges (graph.py:111-148) on the GPU: the same CSR (symmetric,
+    deduplicated, loop-free, columns sorted within rows).  u, v: int64
+    endpoint arrays (numpy or torch).  Returns a host Graph plus the device
+    CSR (offsets int64, columns int64) for chaining."""
+    torch = _lib.torch_cuda()
+    ut = torch.as_tensor(u, dtype=torch.int64).cuda()
+    vt = torch.as_tensor(v, dtype=torch.int64).cuda()
+    keep = ut != vt
+    lo = torch.minimum(ut, vt)[keep]
+    hi = torch.maximum(ut, vt)[keep]
+    del ut, vt, keep
+    und = torch.unique(lo * n + hi)
+    del lo, hi
+    lo, hi = und // n, und % n
+    del und
+    keys, _ = torch.sort(torch.cat([lo * n + hi, hi * n + lo]))
+    del lo, hi
+    src = keys // n
+    dst = keys % n
+    del keys
+    off = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+    off[1:] = torch.cumsum(torch.bincount(src, minlength=n), 0)
+    if original_ids is None:
+        original_ids = np.arange(n, dtype=np.int64)
+    g = Graph(n=n, row_offsets=off.cpu().numpy(), col_indices=dst.cpu().numpy(),
+              original_ids=np.asarray(original_ids, dtype=np.int64))
+    return g, (off, dst, src)
+
+
+def largest_connected_component_device(g, dev=None):
+    """largest_connected_component (graph.py:232-261) with the components
+    computed by kz_connected_components (hook + pointer jumping, labels =
+    smallest node id) and the relabelled CSR built on the device."""
+    torch = _lib.torch_cuda()
+    lib = _lib.load()
+    n = g.n
+    if dev is None:
+        off = torch.as_tensor(g.row_offsets, dtype=torch.int64).cuda()
+        dst = torch.as_tensor(g.col_indices, dtype=torch.int64).cuda()
+        src = torch.repeat_interleave(torch.arange(n, device="cuda"), off[1:] - off[:-1])
+    else:
+        off, dst, src = dev
+    labels = torch.empty(n, dtype=torch.int32, device="cuda")
+    s32 = src.to(torch.int32)
+    d32 = dst.to(torch.int32)
+    _lib.check(lib.kz_connected_components(n, int(d32.numel()), _lib.ptr(s32), _lib.ptr(d32), _lib.ptr(labels),
+                                           _lib.stream_ptr(torch)))
+    del s32, d32
+    lab = labels.to(torch.int64)
+    sizes = torch.bincount(lab, minlength=n)
+    big = int(sizes.max().item())
+    if big == n:
+        return g
+    # largest size; ties -> the component whose smallest id (its label) is smallest
+    best = int(torch.nonzero(sizes == big)[0].item())
+    keep = torch.nonzero(lab == best).flatten()
+    remap = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    remap[keep] = torch.arange(keep.numel(), device="cuda")
+    mask = lab[src] == best
+    cols = remap[dst[mask]]
+    deg = (off[1:] - off[:-1])[keep]
+    new_off = torch.zeros(keep.numel() + 1, dtype=torch.int64, device="cuda")
+    new_off[1:] = torch.cumsum(deg, 0)
+    keep_h = keep.cpu().numpy()
+    return Graph(n=int(keep.numel()), row_offsets=new_off.cpu().numpy(), col_indices=cols.cpu().numpy(),
+                 original_ids=g.original_ids[keep_h].copy())
+
+
 def hardest_alpha(norm):
     """1/(norm + 1) (graph.py:300-308)."""
     if norm < 0:
