@@ -4,11 +4,21 @@ Drop-in for the query side of lrckatz (reference __init__.py:9-72): load a
 KLRC index built by the reference and answer ``query`` (LRC-Katz Schur
 PCG), ``query_cg_baseline`` (plain CG), ``katz_rank`` and ``sparse_katz``
 on one GPU through libkatzb200.so (hand-written sm_100a kernels).  Batched
-variants (``*_batch``) solve many queries per device call.  The offline
-index build, partitioner, recall harness and CLI of the reference are out
-of scope.
+variants (``*_batch``) solve many queries per device call; the recall
+harness (``temporal_split``, ``evaluate_recall[_sweep]``) runs on the
+batched rankers and graph ingestion (``from_edges``, components) has a
+device path.  The offline index build, partitioner and CLI of the reference
+are out of scope.
 """
 
+from .evaluate import (
+    EmptyPositivesError,
+    LinkPredDataset,
+    RecallStat,
+    evaluate_recall,
+    evaluate_recall_sweep,
+    temporal_split,
+)
 from .factor import (
     BlockCholesky,
     DenseCholesky,
