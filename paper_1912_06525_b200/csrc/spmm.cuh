@@ -104,6 +104,17 @@ __device__ __forceinline__ void st_plain(double* p, const double (&v)[VEC]) {
     }
 }
 
+// streaming (evict-first) store: the output block must not push gathered
+// rows out of L2 (column indices are read with __ldcs for the same reason)
+template <int VEC>
+__device__ __forceinline__ void st_stream(double* p, const double (&v)[VEC]) {
+    if constexpr (VEC == 2) {
+        __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    } else {
+        __stcs(p, v[0]);
+    }
+}
+
 // Sum Xg rows of neighbours col[beg..end) into acc, R neighbours per round,
 // rounds `stride` apart.  All lanes of a group share the neighbour; lane lg
 // owns columns lg*VEC .. lg*VEC+VEC-1 of the chunk.  W: weighted operator.
@@ -124,7 +135,7 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
     for (int m = 0; m < K::PER; ++m) {
         const int pos = beg + lg + K::G * m;
         const bool ok = pos < end && (!K::PART || lg < K::R);
-        nidx[m] = ok ? __ldg(col + pos) : 0;
+        nidx[m] = ok ? __ldcs(col + pos) : 0;
         if constexpr (W) nwv[m] = ok ? __ldg(vals + pos) : 0.0;
     }
     const double* __restrict__ Xl = Xc + lg * K::VEC;
@@ -136,7 +147,7 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
             if constexpr (W) wv[m] = nwv[m];
             const int pos = base + stride + lg + K::G * m;
             const bool ok = pos < end && (!K::PART || lg < K::R);
-            nidx[m] = ok ? __ldg(col + pos) : 0;
+            nidx[m] = ok ? __ldcs(col + pos) : 0;
             if constexpr (W) nwv[m] = ok ? __ldg(vals + pos) : 0.0;
         }
         double v[K::R][K::VEC];
@@ -326,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(a.s0, z[q]), y[q]);
             }
-            st_plain<VEC>(a.Y + static_cast<size_t>(chunk) * a.ldy + roff, y);
+            st_stream<VEC>(a.Y + static_cast<size_t>(chunk) * a.ldy + roff, y);
             if (a.want_dot) {
                 double d[VEC];
                 ld_plain<VEC>(a.D ? a.D + static_cast<size_t>(chunk) * a.ldd + roff

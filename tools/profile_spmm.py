@@ -18,10 +18,14 @@ ap.add_argument("--config", default="cfg2")
 ap.add_argument("--b", type=int, default=64)
 ap.add_argument("--chunk", type=int, default=16)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--rcm", action="store_true", help="solve-order operator of GraphIndex (RCM)")
+ap.add_argument("--order", default=None, help="GraphIndex reorder mode (rcm | degree)")
 a = ap.parse_args()
 spec = G.CONFIGS[a.config]
 g = G.rmat_graph_fast(spec["scale"]) if spec["kind"] == "rmat" else G.config_graph(a.config)
-op = kz.DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
+mode = "rcm" if a.rcm else a.order
+op = (kz.GraphIndex(g, 1e-4, reorder=mode).operator() if mode
+      else kz.DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n))
 X = torch.randn(a.b * g.n, dtype=torch.float64, device="cuda")
 Y = torch.empty_like(X)
 dots = torch.empty(a.b, dtype=torch.float64, device="cuda")
