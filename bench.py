@@ -260,6 +260,9 @@ def main():
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(prof):
         traffic = json.load(open(prof)).get("spmm_dram_bytes_per_launch")
+    # actual DRAM traffic (ncu, committed under profiles/) over this run's
+    # CUDA-event launch time: the north-star ">= 60% of peak HBM" view
+    dram_frac = (traffic / (spmm_ms / 1e3) / 1e9 / peak) if traffic else None
     cg_iter_ms = solve_ms / args.steps / max(1.0, float(np.max(iters_all)))
 
     cpu = None
@@ -294,6 +297,9 @@ def main():
                     "api": "paper_1912_06525_b200.katz_rank_batch (host ids in, host ranked lists out)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": f"spmm_kernel<{C}>",
+                         "dram_traffic_frac": dram_frac,
+                         "gathered_bytes_per_launch": 8.0 * nnz * b,
+                         "gathered_tbs": 8.0 * nnz * b / (spmm_ms / 1e3) / 1e12,
                          "algorithmic_bytes_per_launch": b_spmm, "launch_ms": spmm_ms,
                          "peak_source": peak_src,
                          "cg_iteration": {"algorithmic_bytes": b_cg, "ms": cg_iter_ms,
