@@ -162,6 +162,7 @@ typedef struct kz_lrc_args {
 #define KZ_LRC_SCHUR 0     /* out = S in1                      (solver.py:113-115) */
 #define KZ_LRC_PRECOND 1   /* out = S~^-1 in1                  (factor.py:322-337) */
 #define KZ_LRC_SCHUR_RHS 2 /* out = in2 - M12' M11^-1 in1      (solver.py:104-110) */
+#define KZ_LRC_CORRECTION 3 /* out = L^-1 M12' M11^-1 M12 L^-T in1 (factor.py:196-202) */
 
 int kz_lrc_create(const kz_lrc_desc* d, kz_lrc** out);
 int kz_lrc_destroy(kz_lrc* h);
@@ -214,6 +215,21 @@ int kz_pearson_rerank(const double* profiles, const double* ref, const int64_t* 
  * endpoints src/dst (int32[nnz], any orientation, duplicates allowed). */
 int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const int32_t* dst,
                             int32_t* labels, void* stream);
+
+/* ---- index build, host side (no device work) -----------------------------
+ * Vertex-separator partition of a connected graph given as a host CSR
+ * (int64 rowptr[n+1], colidx[nnz], symmetric, no self loops): the
+ * reference's partition_vertex_separator (partition.py:178-248) with its
+ * tie rules, so perm / bounds are identical to the reference's.
+ * limit = PartitionConfig.resolved_part_size(n) (partition.py:40-45),
+ * max_depth = max_recursion_depth.  perm[n] and bounds[n+1] are caller
+ * allocated; bounds[0..*num_parts] are written. */
+int kz_partition(int64_t n, const int64_t* rowptr, const int64_t* colidx, int64_t limit,
+                 int64_t max_depth, int64_t* perm, int64_t* bounds, int64_t* num_parts,
+                 int64_t* n1, int64_t* n2);
+/* Greedy minimum-degree elimination order of one part (factor.py:31-55),
+ * ties to the smallest index; local CSR of the part's internal edges. */
+int kz_min_degree_order(int64_t m, const int64_t* rowptr, const int64_t* colidx, int64_t* order);
 
 /* ---- vector helpers used by the generic cg() / lrc_pcg() drivers -------- */
 /* out[j] = sum_i X[i,j]*Y[i,j] over b columns of length n (column-major). */

@@ -7,9 +7,19 @@ on one GPU through libkatzb200.so (hand-written sm_100a kernels).  Batched
 variants (``*_batch``) solve many queries per device call; the recall
 harness (``temporal_split``, ``evaluate_recall[_sweep]``) runs on the
 batched rankers and graph ingestion (``from_edges``, components) has a
-device path.  The offline index build, partitioner and CLI of the reference
-are out of scope.
+device path.  ``build_index`` builds a KLRC index on the device (native
+partitioner, cuSOLVER separator factor, device Lanczos; build.py) for
+graphs whose CPU build is out of reach.  The CLI of the reference is out of
+scope.
 """
+
+from .build import (
+    DisconnectedGraphError,
+    PartitionConfig,
+    build_index,
+    lanczos_topk,
+    partition_vertex_separator,
+)
 
 from .evaluate import (
     EmptyPositivesError,

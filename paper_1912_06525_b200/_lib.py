@@ -173,6 +173,9 @@ def _declare(lib):
     lib.kz_lrc_workspace_bytes.restype = sz
     lib.kz_lrc_batch.argtypes = [vp, c.POINTER(KzLrcArgs), vp, sz, vp]
     lib.kz_lrc_apply.argtypes = [vp, i32, i32, vp, vp, vp, vp, sz, vp]
+    pi64 = c.POINTER(i64)
+    lib.kz_partition.argtypes = [i64, vp, vp, i64, i64, vp, vp, pi64, pi64, pi64]
+    lib.kz_min_degree_order.argtypes = [i64, vp, vp, vp]
 
 
 def error_from_status(code, lib=None):

@@ -555,6 +555,30 @@ extern "C" int kz_lrc_apply(const kz_lrc* h, int32_t op, int32_t b, const double
             return cx.spmm(h->a21, w.w1, n1, nullptr, 0, in2, n2, out, n2, 1.0, 0.0, h->beta, nullptr, 0, false,
                            nullptr, nullptr);
         }
+        case KZ_LRC_CORRECTION: {
+            // R v = L^-1 M12' M11^-1 M12 L^-T v with M12 = -beta*A12
+            // (factor.py:196-202); the Lanczos operator of the index build.
+            if (n1 == 0) {
+                KZ_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * n2 * b, st));
+                return KZ_OK;
+            }
+            const int64_t l1 = n1, l2 = n2;
+            int rc;
+            // launch_dense(A) applies A' (column-major view of the row-major
+            // operand): the linv buffer gives L^-T, linvT gives L^-1
+            if ((rc = launch_dense(h->linv, h->ld2, n2, n2, 1, in1, l2, w.t2, l2, 1.0, 0.0, 1, b, w.ds, st)))
+                return rc;
+            if ((rc = cx.spmm(h->a12, w.t2, l2, nullptr, 0, nullptr, 0, w.t1, l1, 0.0, 0.0, -h->beta, nullptr, 0,
+                              false, nullptr, nullptr)))
+                return rc;
+            if ((rc = cx.spmm(h->minv, w.t1, l1, nullptr, 0, nullptr, 0, w.w1, l1, 0.0, 0.0, 1.0, nullptr, 0, false,
+                              nullptr, nullptr)))
+                return rc;
+            if ((rc = cx.spmm(h->a21, w.w1, l1, nullptr, 0, nullptr, 0, w.q, l2, 0.0, 0.0, -h->beta, nullptr, 0,
+                              false, nullptr, nullptr)))
+                return rc;
+            return launch_dense(h->linvT, h->ld2, n2, n2, 2, w.q, l2, out, l2, 1.0, 0.0, 1, b, w.ds, st);
+        }
         default:
             return fail(KZ_EARG, "unknown LRC op");
     }

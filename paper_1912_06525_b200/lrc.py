@@ -110,13 +110,17 @@ class DeviceLRC:
         self.t_linv = self.t_linvT = self.t_u = self.t_udT = None
         sigma = np.ascontiguousarray(idx.lr.values[:ell], dtype=np.float64)
         if n2 > 0:
-            lf = np.asarray(idx.dc.factor, dtype=np.float64)
-            linv, info = lapack.dtrtri(lf, lower=1)
-            if info != 0:
-                raise RuntimeError("separator factor is singular")
-            linv = np.tril(linv)
-            self.t_linv = dev(linv)
-            self.t_linvT = dev(linv.T)
+            cache = idx._op_cache()
+            if "linv_pad" in cache:  # device-built index (build.py): L^-1 never left HBM
+                self.t_linv, self.t_linvT = cache["linv_pad"], cache["linvT_pad"]
+            else:
+                lf = np.asarray(idx.dc.factor, dtype=np.float64)
+                linv, info = lapack.dtrtri(lf, lower=1)
+                if info != 0:
+                    raise RuntimeError("separator factor is singular")
+                linv = np.tril(linv)
+                self.t_linv = dev(linv)
+                self.t_linvT = dev(linv.T)
             if ell > 0:
                 u = np.asarray(idx.lr.vectors, dtype=np.float64)[:, :ell]
                 with np.errstate(divide="ignore"):
@@ -234,6 +238,20 @@ class DeviceLRC:
         _lib.check(lib.kz_lrc_apply(self.handle, op, 1, _lib.ptr(a), _lib.ptr(b2), _lib.ptr(out),
                                     _lib.ptr(ws), ws.numel(), _lib.stream_ptr(torch)))
         return out[0].cpu().numpy()
+
+    def apply_correction_device(self, v):
+        """R v (factor.py:196-202) for a device vector of length n2."""
+        torch = _lib.torch_cuda()
+        lib = self.lib
+        a = v.reshape(1, -1).contiguous()
+        out = torch.empty((1, self.n2), dtype=torch.float64, device="cuda")
+        ws = _lib.Workspace.get(torch, lib.kz_lrc_workspace_bytes(self.handle, 1, 1), slot="lrc_apply")
+        _lib.check(lib.kz_lrc_apply(self.handle, 3, 1, _lib.ptr(a), None, _lib.ptr(out),
+                                    _lib.ptr(ws), ws.numel(), _lib.stream_ptr(torch)))
+        return out[0]
+
+    def apply_correction(self, v):
+        return self._apply(3, v, None, self.n2)
 
     def apply_schur(self, v):
         return self._apply(0, v, None, self.n2)

@@ -1,0 +1,214 @@
+"""Index build against the reference's own builds.
+
+The golden KLRC files were written by the reference's build_index
+(tests/golden/make_golden.py, make_recall_golden.py); each test rebuilds the
+same graph with the same parameters and compares:
+
+* CPU: partition (perm, part boundaries, n1/n2, overflow flag), M12, the
+  per-part min-degree orders and Cholesky factors -- byte-exact (the native
+  partitioner and the host part factorisation restate the reference's);
+* GPU: the dense separator factor L (cuSOLVER; rel 1e-12), the Lanczos
+  correction values (abs 1e-10) and spanned subspace, and LRC query scores
+  computed through the rebuilt index against the reference's recorded
+  scores (rel L2 1e-10, iterations +/-1); a save/load round trip; and
+  determinism of the device build.
+"""
+
+import io
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+# (name, requested ell, max_part_size, seed) as in make_golden.py:36-50 and
+# make_recall_golden.py:35
+CASES = [
+    ("k2", 25, None, 7),
+    ("p4", 25, None, 7),
+    ("p5split", 25, 2, 7),
+    ("star5", 25, None, 7),
+    ("triangle", 25, None, 7),
+    ("er40", 4, 8, 7),
+    ("er60", 6, 8, 7),
+    ("ba300", 16, 24, 7),
+    ("ba1200", 25, None, 7),
+    ("recall", 8, 60, 0),
+]
+NAMES = [c[0] for c in CASES]
+PARAMS = {c[0]: c[1:] for c in CASES}
+
+
+@pytest.fixture(scope="module")
+def kz():
+    import paper_1912_06525_b200 as kz
+
+    if kz._lib.load(require=False) is None:
+        pytest.skip("libkatzb200.so not built")
+    return kz
+
+
+def ref_index(kz, name):
+    return kz.load_index(os.path.join(GOLDEN, f"{name}.klrc"))
+
+
+def graph_of(kz, idx):
+    off, col = idx.adjacency_internal()
+    return kz.Graph(n=idx.n, row_offsets=off, col_indices=col.astype(np.int64), original_ids=idx.id_map.copy())
+
+
+def cfg_of(kz, name):
+    mps = PARAMS[name][1]
+    return kz.PartitionConfig(max_part_size=mps) if mps is not None else None
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_partition_matches_reference_build(kz, name):
+    ref = ref_index(kz, name)
+    g = graph_of(kz, ref)
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        bp = kz.partition_vertex_separator(g, cfg_of(kz, name))
+    assert bp.n1 == ref.n1 and bp.n2 == ref.n2
+    assert np.array_equal(bp.perm, ref.bp.perm)
+    assert np.array_equal(bp.part_boundaries, ref.bp.part_boundaries)
+    assert bp.separator_overflow == ref.bp.separator_overflow
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_part_factors_match_reference_bytes(kz, name):
+    from paper_1912_06525_b200 import build as B
+
+    ref = ref_index(kz, name)
+    g = graph_of(kz, ref)
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        bp = kz.partition_vertex_separator(g, cfg_of(kz, name))
+    off, col = B._permuted_adjacency(g, bp)
+    bc = B.block_cholesky(off, col, ref.alpha, bp.part_boundaries)
+    assert bc.num_blocks == ref.bc.num_blocks
+    for b in range(bc.num_blocks):
+        assert np.array_equal(bc.orders[b], ref.bc.orders[b]), b
+        f, r = bc.factors[b], ref.bc.factors[b]
+        assert np.array_equal(f.indptr, r.indptr) and np.array_equal(f.indices, r.indices), b
+        assert f.data.tobytes() == r.data.tobytes(), b
+    o12, c12 = B._sub_pattern(off, col, 0, bp.n1, bp.n1, bp.n)
+    assert np.array_equal(o12, ref.m12.indptr) and np.array_equal(c12, ref.m12.indices)
+    assert np.all(ref.m12.data == -ref.alpha)
+
+
+def test_partition_rejects_disconnected_graph(kz):
+    g = kz.from_edges([(0, 1), (2, 3)])
+    with pytest.raises(kz.DisconnectedGraphError):
+        kz.partition_vertex_separator(g)
+
+
+def test_partition_config_validation(kz):
+    with pytest.raises(ValueError):
+        kz.PartitionConfig(max_part_size=0).resolved_part_size(10)
+    assert kz.PartitionConfig().resolved_part_size(100000) == 390
+    assert kz.PartitionConfig().resolved_part_size(1000) == 64
+
+
+# --------------------------------------------------------------------------- GPU
+_built = {}
+
+
+def built(kz, name):
+    if name not in _built:
+        import warnings
+
+        ref = ref_index(kz, name)
+        ell, _, seed = PARAMS[name]
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            idx = kz.build_index(graph_of(kz, ref), alpha=ref.alpha, ell=ell, cfg=cfg_of(kz, name), seed=seed,
+                                 spectral_norm=ref.spectral_norm)
+        _built[name] = (ref, idx)
+    return _built[name]
+
+
+@pytest.fixture(scope="module")
+def gpu(kz):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return kz
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_device_build_factors(gpu, name):
+    ref, idx = built(gpu, name)
+    assert idx.n2 == ref.n2 and idx.lr.ell == ref.lr.ell
+    if ref.n2:
+        lf, lr_ = idx.dc.factor, ref.dc.factor
+        assert np.linalg.norm(lf - lr_) <= 1e-12 * np.linalg.norm(lr_)
+        assert np.allclose(idx.lr.values, ref.lr.values, rtol=0, atol=1e-10)
+    if ref.lr.ell:
+        # same invariant subspace: singular values of U_ref' U are all ~1
+        s = np.linalg.svd(ref.lr.vectors.T @ idx.lr.vectors, compute_uv=False)
+        assert np.all(s > 1 - 1e-8), s.min()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", [n for n in NAMES if n != "recall"])
+@pytest.mark.parametrize("tol", [1e-8, 1e-10])
+def test_queries_through_device_built_index(gpu, name, tol):
+    ref, idx = built(gpu, name)
+    rec = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    key = f"lrc_{tol:.0e}"
+    scores, reps = gpu.query_batch(idx, rec["queries"], tol=tol)
+    for j in range(len(rec["queries"])):
+        assert abs(reps[j].iterations - rec[f"{key}_iters"][j]) <= 1, (j, reps[j])
+        want = rec[f"{key}_scores"][j]
+        nb = np.linalg.norm(want)
+        assert np.linalg.norm(scores[j] - want) <= 1e-10 * (nb if nb else 1.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["er60", "ba300"])
+def test_device_build_roundtrip_and_determinism(gpu, name):
+    from oracle import katz_oracle as O
+
+    ref, idx = built(gpu, name)
+    a, b = io.BytesIO(), io.BytesIO()
+    gpu.save_index(idx, a)
+    again = gpu.load_index(io.BytesIO(a.getvalue()))
+    assert np.array_equal(again.bp.perm, idx.bp.perm)
+    assert np.array_equal(again.dc.factor, idx.dc.factor)
+    assert np.array_equal(again.lr.vectors, idx.lr.vectors)
+    # the oracle's independent KLRC reader accepts the file
+    path = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"kz_build_{name}.klrc")
+    with open(path, "wb") as fh:
+        fh.write(a.getvalue())
+    O.read_klrc(path)
+    ell, _, seed = PARAMS[name]
+    idx2 = gpu.build_index(graph_of(gpu, ref), alpha=ref.alpha, ell=ell, cfg=cfg_of(gpu, name), seed=seed,
+                           spectral_norm=ref.spectral_norm)
+    gpu.save_index(idx2, b)
+    assert a.getvalue() == b.getvalue()
+
+
+@pytest.mark.gpu
+def test_cfg1_device_built_index_matches_reference_queries(gpu):
+    """BASELINE config 1 built on the device (no reference index needed)
+    and queried: LRC scores/iterations against the reference's own build
+    and query (tests/golden/cfg1_ref.npz, make_cfg1.py)."""
+    from paper_1912_06525_b200.generators import chung_lu_graph
+
+    rec = np.load(os.path.join(GOLDEN, "cfg1_ref.npz"))
+    g = chung_lu_graph()
+    idx = gpu.build_index(g, alpha=float(rec["alpha"]), ell=32, seed=0, spectral_norm=float(rec["spectral_norm"]))
+    assert idx.n2 == int(rec["n2"])
+    scores, reps = gpu.query_batch(idx, rec["queries"], tol=1e-8)
+    for j in range(len(rec["queries"])):
+        assert abs(reps[j].iterations - rec["lrc_iters"][j]) <= 1
+        want = rec["lrc_scores"][j]
+        assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
