@@ -230,6 +230,11 @@ int kz_partition(int64_t n, const int64_t* rowptr, const int64_t* colidx, int64_
 /* Greedy minimum-degree elimination order of one part (factor.py:31-55),
  * ties to the smallest index; local CSR of the part's internal edges. */
 int kz_min_degree_order(int64_t m, const int64_t* rowptr, const int64_t* colidx, int64_t* order);
+/* The orders of all parts in one call: part p is rows [bounds[p], bounds[p+1])
+ * of the partition-ordered adjacency (global columns; entries leaving the
+ * part are ignored); orders[bounds[p] + k] = k-th eliminated local index. */
+int kz_min_degree_orders(int64_t nparts, const int64_t* bounds, const int64_t* rowptr,
+                         const int64_t* colidx, int64_t* orders);
 
 /* ---- vector helpers used by the generic cg() / lrc_pcg() drivers -------- */
 /* out[j] = sum_i X[i,j]*Y[i,j] over b columns of length n (column-major). */

@@ -176,6 +176,7 @@ def _declare(lib):
     pi64 = c.POINTER(i64)
     lib.kz_partition.argtypes = [i64, vp, vp, i64, i64, vp, vp, pi64, pi64, pi64]
     lib.kz_min_degree_order.argtypes = [i64, vp, vp, vp]
+    lib.kz_min_degree_orders.argtypes = [i64, vp, vp, vp, vp]
 
 
 def error_from_status(code, lib=None):

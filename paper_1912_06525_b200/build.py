@@ -39,7 +39,8 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _lib
-from .factor import BlockCholesky, DenseCholesky, FactorizationError, LowRankCorrection, SpectrumError
+from .factor import (BlockCholesky, DenseCholesky, FactorizationError, LazyFactors, LowRankCorrection,
+                     SpectrumError)
 from .graph import InadmissibleAlphaError, KatzParams, hardest_alpha, spectral_norm as _spectral_norm
 from .index import BlockPartition, KatzIndex, permute_csr
 
@@ -135,35 +136,48 @@ def block_cholesky(off, col, alpha, bounds):
     """Per-part min-degree orders and Cholesky factors of M11 = I - alpha*A11
     (factor.py:127-152); parts of equal size are factored in one batched
     LAPACK call (the same per-matrix potrf as the reference's)."""
+    bounds = np.asarray(bounds, dtype=np.int64)
     nparts = bounds.size - 1
-    orders, dense = [None] * nparts, [None] * nparts
-    by_size = {}
-    for p in range(nparts):
-        s, e = int(bounds[p]), int(bounds[p + 1])
-        o, c = _sub_pattern(off, col, s, e, s, e)
-        order = min_degree_order(o, c)
-        orders[p] = order
-        m = e - s
-        a = np.eye(m)
-        pos = np.empty(m, dtype=np.int64)
-        pos[order] = np.arange(m)
-        rows = np.repeat(np.arange(m), np.diff(o))
-        a[pos[rows], pos[c]] = -alpha
-        by_size.setdefault(m, []).append((p, a))
-    for m, items in by_size.items():
-        stack = np.stack([a for _, a in items])
+    n1 = int(bounds[-1])
+    lib = _lib.load()
+    rp = np.ascontiguousarray(off, dtype=np.int64)
+    ci = np.ascontiguousarray(col, dtype=np.int64)
+    flat = np.empty(max(n1, 1), dtype=np.int64)
+    _lib.check(lib.kz_min_degree_orders(nparts, _ptr(bounds), _ptr(rp), _ptr(ci), _ptr(flat)))
+    sizes = np.diff(bounds)
+    part_of = np.repeat(np.arange(nparts), sizes)
+    start = bounds[:-1]
+    # elimination position of every interior node inside its part
+    pos = np.empty(n1, dtype=np.int64)
+    pos[start[part_of] + flat[:n1]] = np.arange(n1) - start[part_of]
+    # interior-interior entries (both ends in the same part by construction)
+    rows = np.repeat(np.arange(n1), np.diff(off[: n1 + 1]))
+    cc = col[: off[n1]]
+    keep = cc < n1
+    rows, cc = rows[keep], cc[keep]
+    orders = [flat[s : s + m].copy() for s, m in zip(start.tolist(), sizes.tolist())]
+    dense = [None] * nparts
+    for m in np.unique(sizes).tolist():
+        members = np.flatnonzero(sizes == m)
+        slot = np.empty(nparts, dtype=np.int64)
+        slot[members] = np.arange(members.size)
+        stack = np.zeros((members.size, m, m))
+        stack[:, np.arange(m), np.arange(m)] = 1.0
+        sel = sizes[part_of[rows]] == m
+        r, c = rows[sel], cc[sel]
+        stack[slot[part_of[r]], pos[r], pos[c]] = -alpha
         try:
             lbs = np.linalg.cholesky(stack)
         except np.linalg.LinAlgError:
-            for p, a in items:  # name the failing part like the reference
+            for k, p in enumerate(members.tolist()):  # name the failing part like the reference
                 try:
-                    np.linalg.cholesky(a)
+                    np.linalg.cholesky(stack[k])
                 except np.linalg.LinAlgError as err:
                     raise FactorizationError(f"part {p} is not positive definite") from err
             raise
-        for (p, _), lb in zip(items, lbs):
-            dense[p] = np.ascontiguousarray(lb)
-    factors = [sp.csr_matrix(lb) for lb in dense]
+        for k, p in enumerate(members.tolist()):
+            dense[p] = lbs[k]
+    factors = LazyFactors(dense)
     return BlockCholesky(block_offsets=np.asarray(bounds, dtype=np.int64), orders=orders, factors=factors,
                          dense=dense)
 
@@ -180,12 +194,14 @@ def _dense_m22(torch, off, col, n1, n, alpha):
     return m22
 
 
-def dense_cholesky_device(torch, m22):
-    """M22 = L L' (factor.py:184-193) and L^-1, on the device."""
+def dense_cholesky_device(torch, off, col, n1, n, alpha):
+    """M22 = L L' (factor.py:184-193) and L^-1, on the device (peak HBM:
+    three n2 x n2 doubles)."""
+    m22 = _dense_m22(torch, off, col, n1, n, alpha)
     lf, info = torch.linalg.cholesky_ex(m22)
+    del m22
     if int(info.item()) != 0:
         raise FactorizationError("separator block is not positive definite")
-    del m22
     eye = torch.eye(lf.shape[0], dtype=torch.float64, device="cuda")
     linv = torch.linalg.solve_triangular(lf, eye, upper=False)
     del eye
@@ -281,19 +297,27 @@ def build_index(g, alpha="hardest", ell=25, cfg=None, seed=0, lanczos_tol=1e-10,
     KatzParams(alpha, norm)
     if alpha < 0.0 or (alpha >= 1.0 and g.num_edges > 0):
         raise InadmissibleAlphaError(f"alpha={alpha} outside the feasible range")
+    stage = {}
+    t = time.perf_counter()
     bp = partition_vertex_separator(g, cfg)
+    stage["partition"] = time.perf_counter() - t
     n, n1, n2 = g.n, bp.n1, bp.n2
     off, col = _permuted_adjacency(g, bp)
     # M12 = -alpha*A12 (build_blocks, partition.py:271-297)
     o12, c12 = _sub_pattern(off, col, 0, n1, n1, n)
     m12 = sp.csr_matrix((np.full(c12.size, -alpha), c12, o12), shape=(n1, n2))
     m12.sort_indices()
+    t = time.perf_counter()
     bc = block_cholesky(off, col, alpha, bp.part_boundaries)
+    stage["part_factors"] = time.perf_counter() - t
     ell_eff = int(min(ell, n2))
     rng = np.random.default_rng(seed)
     linv = None
+    t = time.perf_counter()
     if n2 > 0:
-        lf, linv = dense_cholesky_device(torch, _dense_m22(torch, off, col, n1, n, alpha))
+        lf, linv = dense_cholesky_device(torch, off, col, n1, n, alpha)
+        torch.cuda.synchronize()
+        stage["separator_factor"] = time.perf_counter() - t
         lfac = lf.cpu().numpy()
         del lf
     else:
@@ -315,6 +339,7 @@ def build_index(g, alpha="hardest", ell=25, cfg=None, seed=0, lanczos_tol=1e-10,
         pad[:, :n2] = linv.T
         cache["linvT_pad"] = pad
         del linv
+    t = time.perf_counter()
     if ell_eff > 0:
         start = rng.standard_normal(n2)
         dev = idx.lrc()  # ell = 0 operands: enough for the correction apply
@@ -324,6 +349,7 @@ def build_index(g, alpha="hardest", ell=25, cfg=None, seed=0, lanczos_tol=1e-10,
     else:
         lr = empty
     idx.lr = lr
+    stage["lanczos"] = time.perf_counter() - t
     nnz11 = int(off[n1] - np.count_nonzero(col[: off[n1]] >= n1))  # off-diagonal entries of A11
     m11_nnz = nnz11 + n1
     idx.build_stats = {
@@ -342,5 +368,6 @@ def build_index(g, alpha="hardest", ell=25, cfg=None, seed=0, lanczos_tol=1e-10,
         "correction_rank": lr.ell,
         "correction_values": [float(s) for s in lr.values],
         "build_seconds": time.perf_counter() - t0,
+        "stage_seconds": stage,
     }
     return idx

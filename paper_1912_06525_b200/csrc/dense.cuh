@@ -332,6 +332,154 @@ __global__ void __launch_bounds__(32 * kDmmaWarps) dense_dmma_kernel(DenseArgs a
     if (threadIdx.x == 0) a.cnt[mt] = 0;
 }
 
+// ---- DMMA with shared-memory staged operands, for the big L^-1 products ---
+// At R-MAT 18 (n2 ~ 55k, 64 columns) the fragment-from-global kernel above
+// re-reads the X block from L2 once per warp (8x the A bytes) and runs at a
+// third of the fp64 tensor rate.  Here a CTA owns 128 output rows (8 warps x
+// 2 m-fragments) and walks its k range in slabs of 32: A (32 x 128) and X
+// (32 x NC) slabs are brought into shared memory by cp.async, double
+// buffered, so X is read from L2 once per CTA and every A fragment feeds NT
+// DMMAs, every X fragment MT.  Rows are padded to 64 bytes mod 128 so the
+// 4 k-rows x 8 doubles of a fragment load hit distinct banks (2 wavefronts).
+constexpr int kD2MT = 2;
+constexpr int kD2Rows = 8 * kD2MT * kDmmaWarps;  // 128 rows per CTA tile
+constexpr int kD2KS = 32;                        // k rows per slab
+constexpr int kD2ALd = kD2Rows + 8;              // 136 doubles
+constexpr int kD2XLd = 64 + 8;                   // 72 doubles
+constexpr size_t kD2Smem = sizeof(double) * 2 * kD2KS * (kD2ALd + kD2XLd);
+constexpr int64_t kD2MinDim = 1024;  // smaller operands keep the fragment kernel
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+template <int C, int NT>
+__global__ void __launch_bounds__(32 * kDmmaWarps, 2) dense_dmma2_kernel(DenseArgs a) {
+    constexpr int NC = 8 * NT;
+    extern __shared__ __align__(16) double d2s[];
+    double* As = d2s;                       // [2][KS][ALd]
+    double* Xs = d2s + 2 * kD2KS * kD2ALd;  // [2][KS][XLd]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int mt = blockIdx.x / a.ksplit, ks = blockIdx.x - mt * a.ksplit;
+    const int64_t i0 = static_cast<int64_t>(mt) * kD2Rows;
+    int64_t k0 = static_cast<int64_t>(ks) * a.kper;
+    int64_t k1 = mn64(a.K, k0 + a.kper);
+    const bool empty = dense_tile_empty(a, i0, k0, k1);
+    if (a.tri == 1) k0 = mx64(k0, i0);            // entries with k < i are stored zeros
+    if (a.tri == 2) k1 = mn64(k1, i0 + kD2Rows);  // entries with k > i are stored zeros
+    __shared__ int is_last;
+    double acc[kD2MT][NT][2];
+#pragma unroll
+    for (int m = 0; m < kD2MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+    const int fr = lane >> 2, fk = lane & 3;
+    if (!empty && k0 < k1) {
+        const int64_t nslab = (k1 - k0 + kD2KS - 1) / kD2KS;
+        auto issue = [&](int64_t s, int buf) {
+            const int64_t kk = k0 + s * kD2KS;
+            double* as = As + buf * kD2KS * kD2ALd;
+            double* xs = Xs + buf * kD2KS * kD2XLd;
+            for (int p = threadIdx.x; p < kD2KS * (kD2Rows / 2); p += 32 * kDmmaWarps) {
+                const int r = p / (kD2Rows / 2), c2 = (p % (kD2Rows / 2)) * 2;
+                const int64_t k = kk + r, i = i0 + c2;
+                const bool ok = k < k1 && i < a.lda;
+                cp_async16(as + r * kD2ALd + c2, ok ? a.A + static_cast<size_t>(k) * a.lda + i : a.A, ok ? 16 : 0);
+            }
+            for (int p = threadIdx.x; p < kD2KS * (NC / 2); p += 32 * kDmmaWarps) {
+                const int r = p / (NC / 2), j = (p % (NC / 2)) * 2;
+                const int64_t k = kk + r;
+                const bool ok = k < k1;
+                const double* src = a.X + static_cast<size_t>(j / C) * a.ldx + static_cast<size_t>(k) * C + (j % C);
+                cp_async16(xs + r * kD2XLd + j, ok ? src : a.X, ok ? 16 : 0);
+            }
+            cp_async_commit();
+        };
+        issue(0, 0);
+        for (int64_t s = 0; s < nslab; ++s) {
+            if (s + 1 < nslab) issue(s + 1, static_cast<int>((s + 1) & 1));
+            else cp_async_commit();
+            cp_async_wait1();
+            __syncthreads();
+            const double* as = As + (s & 1) * kD2KS * kD2ALd + warp * (8 * kD2MT) + fr;
+            const double* xs = Xs + (s & 1) * kD2KS * kD2XLd + fr;
+#pragma unroll
+            for (int st = 0; st < kD2KS / 4; ++st) {
+                const int kr = st * 4 + fk;
+                double av[kD2MT], bv[NT];
+#pragma unroll
+                for (int m = 0; m < kD2MT; ++m) av[m] = as[kr * kD2ALd + m * 8];
+#pragma unroll
+                for (int n = 0; n < NT; ++n) bv[n] = xs[kr * kD2XLd + n * 8];
+#pragma unroll
+                for (int m = 0; m < kD2MT; ++m)
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], av[m], bv[n]);
+            }
+            __syncthreads();
+        }
+    }
+    auto store = [&](const double (&v)[kD2MT][NT][2]) {
+#pragma unroll
+        for (int m = 0; m < kD2MT; ++m) {
+            const int64_t row = i0 + warp * (8 * kD2MT) + m * 8 + fr;
+            if (row >= a.M) continue;
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = n * 8 + 2 * fk + e;
+                    double* yp = a.Y + static_cast<size_t>(j / C) * a.ldy + static_cast<size_t>(row) * C + (j % C);
+                    const double s = a.alpha * v[m][n][e];
+                    *yp = a.beta != 0.0 ? fma(a.beta, *yp, s) : s;
+                }
+        }
+    };
+    if (a.ksplit == 1) {
+        store(acc);
+        return;
+    }
+    constexpr int PER = kD2MT * NT * 2;
+    double* mine = a.part + ((static_cast<size_t>(mt) * a.ksplit + ks) * (32 * kDmmaWarps) + threadIdx.x) * PER;
+    if (!empty) {
+#pragma unroll
+        for (int m = 0; m < kD2MT; ++m)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                mine[(m * NT + n) * 2] = acc[m][n][0];
+                mine[(m * NT + n) * 2 + 1] = acc[m][n][1];
+            }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(a.cnt + mt, 1) == a.ksplit - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double tot[kD2MT][NT][2];
+#pragma unroll
+    for (int m = 0; m < kD2MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) tot[m][n][0] = tot[m][n][1] = 0.0;
+    for (int sidx = 0; sidx < a.ksplit; ++sidx) {
+        const int64_t s0 = static_cast<int64_t>(sidx) * a.kper, s1 = mn64(a.K, s0 + a.kper);
+        if (dense_tile_empty(a, i0, s0, s1)) continue;
+        const double* src = a.part + ((static_cast<size_t>(mt) * a.ksplit + sidx) * (32 * kDmmaWarps) + threadIdx.x) * PER;
+#pragma unroll
+        for (int m = 0; m < kD2MT; ++m)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                tot[m][n][0] += __ldcg(src + (m * NT + n) * 2);
+                tot[m][n][1] += __ldcg(src + (m * NT + n) * 2 + 1);
+            }
+    }
+    store(tot);
+    if (threadIdx.x == 0) a.cnt[mt] = 0;
+}
+
 struct DenseScratch {
     double* part = nullptr;
     int32_t* cnt = nullptr;
@@ -353,7 +501,7 @@ inline void dense_plan(int64_t M, int64_t K, int& mtiles, int& ksplit, int64_t& 
 inline size_t dense_part_doubles(int64_t M, int64_t K, int NC) {
     size_t best = 0;
     for (int64_t rows : {static_cast<int64_t>(kDenseThreads), static_cast<int64_t>(kDenseRows),
-                         static_cast<int64_t>(kDmmaRows)}) {
+                         static_cast<int64_t>(kDmmaRows), static_cast<int64_t>(kD2Rows)}) {
         int mtiles, ksplit;
         int64_t kper;
         dense_plan(M, K, mtiles, ksplit, kper, rows);
@@ -378,6 +526,55 @@ inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int 
     };
     for (int c0 = 0, g = 0; c0 < nch; c0 += g) {
         g = group(nch - c0);
+        if (C >= 8 && (C * g) % 8 == 0 && M >= kD2MinDim && K >= kD2MinDim) {
+            const int nt = C * g / 8;
+            int mtiles, ksplit;
+            int64_t kper;
+            dense_plan(M, K, mtiles, ksplit, kper, kD2Rows);
+            DenseArgs a{};
+            a.rows_tile = kD2Rows;
+            a.A = A;
+            a.lda = lda;
+            a.M = M;
+            a.K = K;
+            a.tri = tri;
+            a.X = X + static_cast<size_t>(c0) * ldx;
+            a.ldx = ldx;
+            a.Y = Y + static_cast<size_t>(c0) * ldy;
+            a.ldy = ldy;
+            a.alpha = alpha;
+            a.beta = beta;
+            a.ksplit = ksplit;
+            a.kper = kper;
+            a.part = ds.part;
+            a.cnt = ds.cnt;
+            if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * kD2Rows * g * C > ds.part_cap ||
+                               mtiles > ds.cnt_cap))
+                return fail(KZ_EARG, "dense scratch too small");
+            const unsigned grid = static_cast<unsigned>(mtiles) * ksplit;
+#define KZ_DMMA2(CC, NN)                                                                                  \
+    do {                                                                                                  \
+        static bool attr = false;                                                                         \
+        if (!attr) {                                                                                      \
+            KZ_CUDA(cudaFuncSetAttribute(dense_dmma2_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         static_cast<int>(kD2Smem)));                                     \
+            attr = true;                                                                                  \
+        }                                                                                                 \
+        dense_dmma2_kernel<CC, NN><<<grid, 32 * kDmmaWarps, kD2Smem, st>>>(a);                            \
+    } while (0)
+            if (C == 8 && nt == 1) KZ_DMMA2(8, 1);
+            else if (C == 16 && nt == 2) KZ_DMMA2(16, 2);
+            else if (C == 16 && nt == 4) KZ_DMMA2(16, 4);
+            else if (C == 16 && nt == 6) KZ_DMMA2(16, 6);
+            else if (C == 16 && nt == 8) KZ_DMMA2(16, 8);
+            else if (C == 32 && nt == 4) KZ_DMMA2(32, 4);
+            else if (C == 32 && nt == 8) KZ_DMMA2(32, 8);
+            else return fail(KZ_EARG, "dmma2: unsupported column group");
+#undef KZ_DMMA2
+            note_launch();
+            KZ_LAUNCH_CHECK();
+            continue;
+        }
         if ((C * g) % 8 == 0) {
             const int nt = C * g / 8;
             int mtiles, ksplit;

@@ -229,17 +229,17 @@ extern "C" int kz_partition(int64_t n, const int64_t* rowptr, const int64_t* col
     return KZ_OK;
 }
 
-// _min_degree_order (factor.py:31-55) of one part: its internal adjacency
-// in local CSR (m nodes).  Elimination simulation on dense boolean rows
-// (parts are small); ties to the smallest index.
-extern "C" int kz_min_degree_order(int64_t m, const int64_t* rowptr, const int64_t* colidx, int64_t* order) {
-    if (m < 0 || (m > 0 && (!rowptr || !order))) return KZ_EARG;
+namespace {
+
+// Minimum-degree elimination of one part whose rows are [s, s+m) of a CSR
+// with global columns (entries outside [s, s+m) are ignored).
+void min_degree_part(int64_t s, int64_t m, const int64_t* rowptr, const int64_t* colidx, int64_t* order) {
     std::vector<std::vector<char>> nb(m, std::vector<char>(m, 0));
     std::vector<int64_t> deg(m, 0);
     for (int64_t i = 0; i < m; ++i)
-        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
-            const int64_t j = colidx[e];
-            if (j != i && !nb[i][j]) {
+        for (int64_t e = rowptr[s + i]; e < rowptr[s + i + 1]; ++e) {
+            const int64_t j = colidx[e] - s;
+            if (j >= 0 && j < m && j != i && !nb[i][j]) {
                 nb[i][j] = 1;
                 ++deg[i];
             }
@@ -266,6 +266,31 @@ extern "C" int kz_min_degree_order(int64_t m, const int64_t* rowptr, const int64
                     nb[x][y] = 1;
                     ++deg[x];
                 }
+    }
+}
+
+}  // namespace
+
+// _min_degree_order (factor.py:31-55) of one part: its internal adjacency
+// in local CSR (m nodes).  Elimination simulation on dense boolean rows
+// (parts are small); ties to the smallest index.
+extern "C" int kz_min_degree_order(int64_t m, const int64_t* rowptr, const int64_t* colidx, int64_t* order) {
+    if (m < 0 || (m > 0 && (!rowptr || !order))) return KZ_EARG;
+    if (m > 0) min_degree_part(0, m, rowptr, colidx, order);
+    return KZ_OK;
+}
+
+// All parts at once: rows [bounds[p], bounds[p+1]) of the partition-ordered
+// adjacency (global columns) form part p; orders[bounds[p] + k] receives the
+// k-th eliminated local index of part p.
+extern "C" int kz_min_degree_orders(int64_t nparts, const int64_t* bounds, const int64_t* rowptr,
+                                    const int64_t* colidx, int64_t* orders) {
+    if (nparts < 0 || (nparts > 0 && (!bounds || !rowptr || !orders))) return KZ_EARG;
+    for (int64_t p = 0; p < nparts; ++p) {
+        const int64_t s = bounds[p], m = bounds[p + 1] - s;
+        if (m < 0) return KZ_EARG;
+        if (m == 1) orders[s] = 0;
+        else if (m > 1) min_degree_part(s, m, rowptr, colidx, orders + s);
     }
     return KZ_OK;
 }

@@ -47,7 +47,34 @@ class BlockCholesky:
 
     @property
     def nnz(self):
-        return int(sum(f.nnz for f in self.factors))
+        return int(sum(np.count_nonzero(d) for d in self.dense))
+
+
+class LazyFactors:
+    """``factors`` of a device-built BlockCholesky: the sparse copy of each
+    dense part factor (sp.csr_matrix(lb), factor.py:148) made on first access,
+    so a build with 10^5 parts does not pay for scipy object construction
+    unless the index is saved or inspected."""
+
+    def __init__(self, dense):
+        self._dense = dense
+        self._cache = {}
+
+    def __len__(self):
+        return len(self._dense)
+
+    def __getitem__(self, b):
+        if isinstance(b, slice):
+            return [self[i] for i in range(*b.indices(len(self)))]
+        f = self._cache.get(b)
+        if f is None:
+            import scipy.sparse as sp
+
+            f = self._cache[b] = sp.csr_matrix(self._dense[b])
+        return f
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
 
 
 @dataclass(eq=False)
