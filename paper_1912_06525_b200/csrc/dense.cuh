@@ -347,7 +347,7 @@ constexpr int kD2KS = 32;                        // k rows per slab
 constexpr int kD2ALd = kD2Rows + 8;              // 136 doubles
 constexpr int kD2XLd = 64 + 8;                   // 72 doubles
 constexpr size_t kD2Smem = sizeof(double) * 2 * kD2KS * (kD2ALd + kD2XLd);
-constexpr int64_t kD2MinDim = 1024;  // smaller operands keep the fragment kernel
+constexpr int64_t kD2MinDim = 8192;  // smaller operands keep the fragment kernel (faster at cfg1, n2 = 5k)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
