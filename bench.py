@@ -2,13 +2,16 @@
 """Benchmark: Katz queries/sec at R-MAT scale-22 (BASELINE.json configs[2]).
 
 One step = one batch of b=256 seeded queries through the hot path: batched
-plain-CG Katz solve (tol 1e-8, beta = 0.5/lambda_max) + masked top-100
-(katz_rank semantics).  The R-MAT LRC index is infeasible for the reference
-(SURVEY.md §0.3), so the headline path is the reference's query_cg_baseline
-/ cg recurrence.  Inputs are seeded synthetic graphs (no dataset), and every
+Katz solve (tol 1e-8, beta = 0.5/lambda_max) + masked top-100 (katz_rank
+semantics).  The default solver is the north-star LRC-Katz: a low-rank term
+from the rank-128 eigen index of A (BASELINE configs[2] r=128; U, AU, W built
+once, outside the timed region, like the reference's offline index) plus the
+CG correction from that start (EigenIndex, kz_eigen_batch); --solver cg runs
+the reference's query_cg_baseline recurrence from zero instead, and the line
+reports both.  Inputs are seeded synthetic graphs (no dataset), and every
 solve vector block (4.9 GB) is far larger than L2, so no flush is needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--solver eigen|cg]
   python bench.py --impl reference ...   # CPU oracle port of the reference path
 
 Multi-GPU: one process per GPU (torchrun), each rank a full replica solving
@@ -46,6 +49,7 @@ def parse():
     ap.add_argument("--config", default="cfg3", choices=["cfg1", "proxy16", "cfg2", "cfg3"])
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver", default="eigen", choices=["eigen", "cg"])
     return ap.parse_args()
 
 
@@ -181,9 +185,20 @@ def main():
     qs = G.sample_queries(g.original_ids, b, seed=rank)
     internal = idx.internal_ids(qs)
     n, nnz = g.n, g.nnz
+    eidx, t_index = None, 0.0
+    if args.solver == "eigen":
+        t1 = time.perf_counter()
+        eidx = kz.EigenIndex(idx, spec["ell"])
+        t_index = time.perf_counter() - t1
+    qidx = eidx if eidx is not None else idx
+
+    def solve():
+        if eidx is not None:
+            return kz.query_batch(eidx, qs, tol=tol, device=True)
+        return kz.query_cg_baseline_batch(idx, qs, tol=tol, device=True)
 
     def step():
-        scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol, device=True)
+        scores, reps = solve()
         ids, vals, counts = kz.topk_device(scores, k, idx.mask_operator(), internal, internal)
         return reps, ids
 
@@ -222,7 +237,7 @@ def main():
     e2e_t = []
     for _ in range(max(1, min(args.steps, 3))):
         t1 = time.perf_counter()
-        preds = kz.katz_rank_batch(idx, qs, k, tol=tol)
+        preds = kz.katz_rank_batch(qidx, qs, k, tol=tol)
         e2e_t.append(time.perf_counter() - t1)
     e2e_s = statistics.median(e2e_t)
     if world > 1:
@@ -265,6 +280,26 @@ def main():
     dram_frac = (traffic / (spmm_ms / 1e3) / 1e9 / peak) if traffic else None
     cg_iter_ms = solve_ms / args.steps / max(1.0, float(np.max(iters_all)))
 
+    # the other solver on the same queries, for the record (not the headline)
+    plain = None
+    if eidx is not None:
+        def cg_step():
+            scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol, device=True)
+            kz.topk_device(scores, k, idx.mask_operator(), internal, internal)
+            return reps
+        cg_step()
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(3):
+            creps = cg_step()
+        c1.record()
+        torch.cuda.synchronize()
+        cms = c0.elapsed_time(c1) / 3
+        plain = {"solver": "plain CG from zero (query_cg_baseline)", "value": b * world / (cms / 1e3),
+                 "ms_per_step": cms, "mean_cg_iterations": float(np.mean([r.iterations for r in creps])),
+                 "max_cg_iterations": int(max(r.iterations for r in creps))}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
@@ -288,8 +323,14 @@ def main():
             "dtype": "f64",
             "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
             "config": {"workload": workload, "n": n, "nnz": nnz, "beta": beta, "lambda_max": lam,
-                       "queries_per_gpu": b, "top_k": k, "tol": tol, "solver": "plain CG (query_cg_baseline)",
-                       "mean_cg_iterations": mean_iters, "l2": "inputs larger than L2 (4.9 GB blocks), no flush",
+                       "queries_per_gpu": b, "top_k": k, "tol": tol,
+                       "solver": (f"LRC-Katz, eigen form: rank-{eidx.rank} eigen index of A (low-rank Galerkin "
+                                  f"term, two fp64 DMMA GEMMs) + CG correction" if eidx is not None
+                                  else "plain CG (query_cg_baseline)"),
+                       "eigen_index_build_s": round(t_index, 2) if eidx is not None else None,
+                       "mean_cg_iterations": mean_iters, "max_cg_iterations": int(np.max(iters_all)),
+                       "plain_cg": plain,
+                       "l2": "inputs larger than L2 (4.9 GB blocks), no flush",
                        "parallelism": f"replicas x{world} (query-column sharding)",
                        "graph_build_s": round(t_graph, 1)},
             "e2e": {"value": b * world / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d,
@@ -303,7 +344,9 @@ def main():
                          "algorithmic_bytes_per_launch": b_spmm, "launch_ms": spmm_ms,
                          "peak_source": peak_src,
                          "cg_iteration": {"algorithmic_bytes": b_cg, "ms": cg_iter_ms,
-                                          "achieved_gbs": b_cg / (cg_iter_ms / 1e3) / 1e9}},
+                                          "achieved_gbs": b_cg / (cg_iter_ms / 1e3) / 1e9,
+                                          "note": "solve time per step / max iterations"
+                                                  + (" (includes the low-rank start)" if eidx is not None else "")}},
             "cpu_baseline": cpu,
             "clocks": clock_info,
             "gpu_launches": int(launches),

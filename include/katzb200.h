@@ -216,6 +216,30 @@ int kz_pearson_rerank(const double* profiles, const double* ref, const int64_t* 
 int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const int32_t* dst,
                             int32_t* labels, void* stream);
 
+/* ---- eigen-of-A low-rank start + CG (north-star LRC) ---
+ * Not in the reference (its LRC is the Schur form above); parity is against
+ * the exact solution.  Index: U = top-r Ritz vectors of A in the operator's
+ * order, AU = A U, W = (I - beta U'AU)^-1.  kz_eigen_batch solves the same
+ * systems as kz_cg_batch (query columns by qpos; rhs and x0 must be NULL)
+ * but starts each column at the Galerkin point x0 = U W U' b with the exact
+ * residual r0 = b - x0 + beta (AU)(W U' b) -- two tall-skinny fp64 DMMA
+ * products, no SpMM -- then runs the reference's CG recurrence from there
+ * with the stop test ||r|| <= tol ||b|| (solver.py:62-101). */
+typedef struct kz_eigen kz_eigen;
+typedef struct kz_eigen_desc {
+    int64_t n, r;
+    int64_t ldr;          /* row stride of u / au: >= r, multiple of 4, zero padded, <= 384 */
+    double beta;
+    const kz_graph* op;   /* A (n x n) in the solve order */
+    const double* u;      /* device n x ldr row-major */
+    const double* au;     /* device n x ldr row-major, A U */
+    const double* w;      /* device r x r row-major, (I - beta U'AU)^-1 */
+} kz_eigen_desc;
+int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out);
+int kz_eigen_destroy(kz_eigen* h);
+size_t kz_eigen_workspace_bytes(const kz_eigen* h, int32_t b);
+int kz_eigen_batch(const kz_eigen* h, const kz_cg_args* a, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- index build, host side (no device work) -----------------------------
  * Vertex-separator partition of a connected graph given as a host CSR
  * (int64 rowptr[n+1], colidx[nnz], symmetric, no self loops): the

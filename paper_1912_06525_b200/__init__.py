@@ -13,6 +13,7 @@ graphs whose CPU build is out of reach.  The CLI of the reference is out of
 scope.
 """
 
+from .eigen import EigenIndex
 from .build import (
     DisconnectedGraphError,
     PartitionConfig,

@@ -120,6 +120,19 @@ class KzLrcArgs(ctypes.Structure):
     ]
 
 
+class KzEigenDesc(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64),
+        ("r", ctypes.c_int64),
+        ("ldr", ctypes.c_int64),
+        ("beta", ctypes.c_double),
+        ("op", ctypes.c_void_p),
+        ("u", ctypes.c_void_p),
+        ("au", ctypes.c_void_p),
+        ("w", ctypes.c_void_p),
+    ]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -177,6 +190,11 @@ def _declare(lib):
     lib.kz_partition.argtypes = [i64, vp, vp, i64, i64, vp, vp, pi64, pi64, pi64]
     lib.kz_min_degree_order.argtypes = [i64, vp, vp, vp]
     lib.kz_min_degree_orders.argtypes = [i64, vp, vp, vp, vp]
+    lib.kz_eigen_create.argtypes = [c.POINTER(KzEigenDesc), c.POINTER(vp)]
+    lib.kz_eigen_destroy.argtypes = [vp]
+    lib.kz_eigen_workspace_bytes.argtypes = [vp, i32]
+    lib.kz_eigen_workspace_bytes.restype = sz
+    lib.kz_eigen_batch.argtypes = [vp, c.POINTER(KzCgArgs), vp, sz, vp]
 
 
 def error_from_status(code, lib=None):

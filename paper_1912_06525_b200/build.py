@@ -221,10 +221,13 @@ def _fresh_direction(torch, rng, basis):
     raise RuntimeError("could not draw a direction outside the current basis")
 
 
-def lanczos_topk(apply, ell, start, max_iter=None, tol=1e-10, rng=None):
+def lanczos_topk(apply, ell, start, max_iter=None, tol=1e-10, rng=None, psd=True, which="LA"):
     """lanczos_topk (factor.py:235-319) with the basis and the operator on
     the device; same step budget, breakdown rule, early stop and restart
-    directions as the reference."""
+    directions as the reference.  psd=False (an indefinite operator such as
+    A itself) skips the reference's non-negativity check and clamp;
+    which="LM" selects the ell Ritz pairs of largest magnitude instead of the
+    largest algebraic values (the reference's choice)."""
     from scipy.linalg import eigh_tridiagonal
 
     torch = _lib.torch_cuda()
@@ -263,7 +266,7 @@ def lanczos_topk(apply, ell, start, max_iter=None, tol=1e-10, rng=None):
                 y = np.ones((1, 1))
             else:
                 theta, y = eigh_tridiagonal(alphas, betas)
-            top = np.argsort(theta)[::-1][:ell]
+            top = np.argsort(np.abs(theta) if which == "LM" else theta)[::-1][:ell]
             resid = b * np.abs(y[-1, top])
             if (np.all(resid <= tol) and not had_breakdown) or j == m:
                 break
@@ -276,9 +279,10 @@ def lanczos_topk(apply, ell, start, max_iter=None, tol=1e-10, rng=None):
     vals = theta[top]
     yt = torch.as_tensor(np.ascontiguousarray(y[:, top]), device="cuda")
     vecs = (basis[:j].T @ yt).cpu().numpy()
-    if np.any(vals < -1e-8):
-        raise SpectrumError(f"negative correction eigenvalue {vals.min():.3e}")
-    vals = np.maximum(vals, 0.0)
+    if psd:
+        if np.any(vals < -1e-8):
+            raise SpectrumError(f"negative correction eigenvalue {vals.min():.3e}")
+        vals = np.maximum(vals, 0.0)
     return LowRankCorrection(ell=int(top.size), vectors=vecs, values=vals)
 
 

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "driver.cuh"
+#include "lowrank.cuh"
 
 using namespace kz;
 
@@ -30,9 +31,10 @@ struct CgWork {
     SolveState st;
     int64_t* qpos;
     int64_t* iperm;  // inverse output permutation (gather-based store)
+    double* y;       // eigen start: [nch][ldr][C] Galerkin coefficients
 };
 
-void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w) {
+void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* eig = nullptr) {
     w.C = default_chunk(b);
     w.nchunks = (b + w.C - 1) / w.C;
     w.bpad = w.nchunks * w.C;
@@ -66,6 +68,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w) {
     s.err = cv.take<int32_t>(1);
     w.qpos = cv.take<int64_t>(w.bpad);
     w.iperm = cv.take<int64_t>(g->rows);
+    w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
 }
 
 
@@ -80,15 +83,18 @@ extern "C" size_t kz_cg_workspace_bytes(const kz_graph* g, int32_t b) {
 }
 
 
-extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, size_t ws_bytes,
-                           void* stream) {
-    clear_error();
+// The batched CG of kz_cg_batch; with `eig` the columns start from the
+// eigen-of-A Galerkin point (lowrank.cuh) instead of zero / x0.
+static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_t ws_bytes, void* stream,
+                         const kz_eigen* eig) {
     if (!g || !a) return fail(KZ_EARG, "NULL argument");
     if (g->rows != g->cols) return fail(KZ_EARG, "CG needs a square operator");
     if (a->b < 1) return fail(KZ_EARG, "empty batch");
     if (!a->scores || !a->reports) return fail(KZ_EARG, "NULL outputs");
     if (!a->rhs && !a->qpos) return fail(KZ_EARG, "need qpos or rhs");
-    if (!ws || ws_bytes < kz_cg_workspace_bytes(g, a->b)) return fail(KZ_EARG, "workspace too small");
+    if (eig && (a->rhs || a->x0 || !a->qpos)) return fail(KZ_EARG, "the eigen start needs query positions only");
+    if (!ws || ws_bytes < (eig ? kz_eigen_workspace_bytes(eig, a->b) : kz_cg_workspace_bytes(g, a->b)))
+        return fail(KZ_EARG, "workspace too small");
     const int b = a->b;
     const int64_t n = g->rows;
     if (a->qpos && !a->rhs)
@@ -98,7 +104,7 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
 
     Carver cv(ws, ws_bytes);
     CgWork w;
-    carve_cg(cv, g, b, w);
+    carve_cg(cv, g, b, w, eig);
     SolveState& s = w.st;
     s.b = b;
     s.bpad = w.bpad;
@@ -137,7 +143,7 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
     KZ_LAUNCH_CHECK();
     // ||b||, optional start vector (solver.py:51-59), init finalize
     KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red,
-                                                                     a->x0 ? FIN_INIT_B : FIN_INIT_BR,
+                                                                     (a->x0 || eig) ? FIN_INIT_B : FIN_INIT_BR,
                                                                      s, nullptr, 0); ::kz::note_launch());
     KZ_LAUNCH_CHECK();
     if (a->x0) {
@@ -153,6 +159,36 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
         sa.s2 = a->beta;  // r = b - (x - beta*A x)
         sa.want_dot = 0;
         if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
+        KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+    }
+    if (eig) {
+        // y = beta W (AU)[q,:]';  x = U y;  r = b - x + beta (AU) y
+        const dim3 cgrid(static_cast<unsigned>((eig->ldr + 127) / 128), static_cast<unsigned>(w.bpad));
+        KZ_DISPATCH_C(C, lowrank_coef_kernel<CC><<<cgrid, 128, 0, st>>>(*eig, w.qpos, b, w.y); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+        const int nt = w.bpad >= 64 ? 8 : w.bpad >= 32 ? 4 : w.bpad >= 16 ? 2 : 1;
+        const size_t smem = lowrank_smem(eig->ldr, 8 * nt);
+        const int64_t ntiles = (n + kLrRows - 1) / kLrRows;
+        const unsigned lgrid = static_cast<unsigned>(std::min<int64_t>(2 * kNumSMs, ntiles));
+        for (int j0 = 0; j0 < w.bpad; j0 += 8 * nt) {
+#define KZ_LR(NN)                                                                                              \
+    do {                                                                                                       \
+        KZ_DISPATCH_C(C, {                                                                                     \
+            KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                         static_cast<int>(smem)));                                             \
+            lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, n * CC, j0,   \
+                                                                            w.bpad);                           \
+            ::kz::note_launch();                                                                               \
+        });                                                                                                    \
+    } while (0)
+            if (nt == 8) KZ_LR(8);
+            else if (nt == 4) KZ_LR(4);
+            else if (nt == 2) KZ_LR(2);
+            else KZ_LR(1);
+#undef KZ_LR
+            KZ_LAUNCH_CHECK();
+        }
         KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
     }
@@ -231,6 +267,54 @@ extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, siz
     }
     if (notspd) return fail(KZ_ENOTSPD, "operator is not positive definite");
     return KZ_OK;
+}
+
+extern "C" int kz_cg_batch(const kz_graph* g, const kz_cg_args* a, void* ws, size_t ws_bytes,
+                           void* stream) {
+    clear_error();
+    return cg_batch_impl(g, a, ws, ws_bytes, stream, nullptr);
+}
+
+// ---- eigen-of-A low-rank start + CG ----------------------
+extern "C" int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out) {
+    clear_error();
+    if (!d || !out) return fail(KZ_EARG, "NULL argument");
+    *out = nullptr;
+    if (!d->op || d->n < 1 || d->r < 1 || d->ldr < d->r || d->ldr % 4 != 0 || !d->u || !d->au || !d->w)
+        return fail(KZ_EARG, "bad eigen index description");
+    if (d->op->rows != d->n || d->op->cols != d->n) return fail(KZ_EARG, "operator size differs from n");
+    if (lowrank_smem(d->ldr, 64) > 227 * 1024) return fail(KZ_EARG, "rank too large (ldr > 384)");
+    auto* h = new kz_eigen();
+    h->n = d->n;
+    h->r = d->r;
+    h->ldr = d->ldr;
+    h->beta = d->beta;
+    h->op = d->op;
+    h->u = d->u;
+    h->au = d->au;
+    h->w = d->w;
+    *out = h;
+    return KZ_OK;
+}
+
+extern "C" int kz_eigen_destroy(kz_eigen* h) {
+    delete h;
+    return KZ_OK;
+}
+
+extern "C" size_t kz_eigen_workspace_bytes(const kz_eigen* h, int32_t b) {
+    if (!h || b < 1) return 0;
+    Carver cv(nullptr, 0);
+    CgWork w;
+    carve_cg(cv, h->op, b, w, h);
+    return cv.off + 256;
+}
+
+extern "C" int kz_eigen_batch(const kz_eigen* h, const kz_cg_args* a, void* ws, size_t ws_bytes, void* stream) {
+    clear_error();
+    if (!h || !a) return fail(KZ_EARG, "NULL argument");
+    if (a->beta != h->beta) return fail(KZ_EARG, "beta differs from the eigen index's");
+    return cg_batch_impl(h->op, a, ws, ws_bytes, stream, h);
 }
 
 extern "C" int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out,

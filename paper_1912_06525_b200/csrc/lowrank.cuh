@@ -1,0 +1,154 @@
+// lowrank.cuh -- the eigen-of-A low-rank start of the north-star LRC variant
+// (not in the reference, parity only against the exact
+// solution).
+//
+// Index: U = n x r Ritz vectors of A (top r, device Lanczos), AU = A U (one
+// K1 SpMM of the r-column block), W = (I - beta U'AU)^-1 (r x r).  For a
+// query q the Galerkin start on span(U) is
+//     x0 = U y,   y = W U' b = beta * W (AU)[q, :]'      (b = beta A e_q)
+// and its exact residual needs no SpMM:
+//     r0 = b - (I - beta A) U y = b - x0 + beta * (AU) y.
+// CG then runs from (x0, r0) with the stop test ||r|| <= tol ||b|| -- the same
+// iterates as CG on M d = r0 from zero.  The two tall-skinny products
+// U y and (AU) y (n x r times r x b) are one fused DMMA pass.
+#pragma once
+
+#include "spmm.cuh"
+
+struct kz_eigen {
+    int64_t n = 0, r = 0, ldr = 0;  // ldr: row stride of u / au (>= r, multiple of 4, zero padded)
+    double beta = 0.0;
+    const kz_graph* op = nullptr;   // A in the solve order
+    const double* u = nullptr;      // device n x ldr row-major
+    const double* au = nullptr;     // device n x ldr row-major
+    const double* w = nullptr;      // device r x r row-major, symmetric
+};
+
+namespace kz {
+
+// y[j] (chunked [nch][ldr][C]) = beta * W (AU)[q_j, :]'; padded columns and
+// rows r..ldr-1 are zero.  One thread per (k, j); fixed summation order.
+template <int C>
+__global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos, int b, double* __restrict__ y) {
+    const int j = blockIdx.y;
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= h.ldr) return;
+    double s = 0.0;
+    if (j < b && k < h.r) {
+        const double* __restrict__ aurow = h.au + qpos[j] * h.ldr;
+        const double* __restrict__ wrow = h.w + k * h.r;
+        for (int64_t i = 0; i < h.r; ++i) s = fma(wrow[i], __ldg(aurow + i), s);
+        s *= h.beta;
+    }
+    y[static_cast<size_t>(j / C) * h.ldr * C + static_cast<size_t>(k) * C + (j % C)] = s;
+}
+
+constexpr int kLrWarps = 8;
+constexpr int kLrMT = 1;                           // m-fragments (8 rows) per warp (2 spills)
+constexpr int kLrRows = 8 * kLrMT * kLrWarps;      // rows per tile
+constexpr int kLrAhead = 4;                        // k-steps of A fragments in flight
+
+__device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// For the NC = 8*NT columns j0 .. j0+NC-1 (the column group; columns >= jmax
+// are padding and are neither read nor written):
+//   x = U y ;  r = (r - x) + beta * (AU y)          (r holds b on entry)
+// y's group columns are staged in shared memory once per CTA ([ldr][NC+8],
+// bank padded); each warp owns 16 rows of a 128-row tile and streams its U
+// and AU fragments from HBM kLrAhead k-steps ahead.  Persistent over tiles.
+template <int C, int NT>
+__global__ void __launch_bounds__(32 * kLrWarps, 2)
+    lowrank_init_kernel(kz_eigen h, const double* __restrict__ y, double* __restrict__ x, double* __restrict__ r,
+                        int64_t ldv, int j0, int jmax) {
+    constexpr int NC = 8 * NT;
+    constexpr int YLD = NC + 8;
+    extern __shared__ __align__(16) double ys[];
+    const int64_t ldr = h.ldr;
+    for (int e = threadIdx.x; e < ldr * NC; e += blockDim.x) {
+        const int k = e / NC, jj = e % NC;
+        const int j = j0 + jj;
+        ys[k * YLD + jj] = j < jmax ? y[static_cast<size_t>(j / C) * ldr * C + static_cast<size_t>(k) * C + (j % C)] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int fr = lane >> 2, fk = lane & 3;
+    const int64_t ntiles = (h.n + kLrRows - 1) / kLrRows;
+    const int nsteps = static_cast<int>(ldr / 4);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t rw = tile * kLrRows + warp * (8 * kLrMT);
+        double ua[kLrMT][NT][2], wa[kLrMT][NT][2];
+#pragma unroll
+        for (int m = 0; m < kLrMT; ++m)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) ua[m][n][0] = ua[m][n][1] = wa[m][n][0] = wa[m][n][1] = 0.0;
+        const double* up[kLrMT];
+        const double* wp[kLrMT];
+#pragma unroll
+        for (int m = 0; m < kLrMT; ++m) {
+            int64_t row = rw + m * 8 + fr;
+            row = row < h.n ? row : h.n - 1;  // clamped rows are computed and not stored
+            up[m] = h.u + row * ldr + fk;
+            wp[m] = h.au + row * ldr + fk;
+        }
+        double fu[kLrAhead][kLrMT], fw[kLrAhead][kLrMT];
+#pragma unroll
+        for (int s = 0; s < kLrAhead; ++s)
+#pragma unroll
+            for (int m = 0; m < kLrMT; ++m) {
+                const bool ok = s < nsteps;
+                fu[s][m] = ok ? __ldcs(up[m] + 4 * s) : 0.0;
+                fw[s][m] = ok ? __ldcs(wp[m] + 4 * s) : 0.0;
+            }
+        for (int s0 = 0; s0 < nsteps; s0 += kLrAhead) {
+#pragma unroll
+            for (int u = 0; u < kLrAhead; ++u) {
+                const int s = s0 + u;
+                double cu[kLrMT], cw[kLrMT];
+#pragma unroll
+                for (int m = 0; m < kLrMT; ++m) {
+                    cu[m] = fu[u][m];
+                    cw[m] = fw[u][m];
+                    const bool ok = s + kLrAhead < nsteps;
+                    fu[u][m] = ok ? __ldcs(up[m] + 4 * (s + kLrAhead)) : 0.0;
+                    fw[u][m] = ok ? __ldcs(wp[m] + 4 * (s + kLrAhead)) : 0.0;
+                }
+                if (s < nsteps) {
+                    double bv[NT];
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) bv[n] = ys[(4 * s + fk) * YLD + n * 8 + fr];
+#pragma unroll
+                    for (int m = 0; m < kLrMT; ++m)
+#pragma unroll
+                        for (int n = 0; n < NT; ++n) {
+                            lr_dmma(ua[m][n][0], ua[m][n][1], cu[m], bv[n]);
+                            lr_dmma(wa[m][n][0], wa[m][n][1], cw[m], bv[n]);
+                        }
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < kLrMT; ++m) {
+            const int64_t row = rw + m * 8 + fr;
+            if (row >= h.n) continue;
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = j0 + n * 8 + 2 * fk + e;
+                    if (j >= jmax) continue;
+                    const size_t off = static_cast<size_t>(j / C) * ldv + static_cast<size_t>(row) * C + (j % C);
+                    const double x0 = ua[m][n][e];
+                    x[off] = x0;
+                    r[off] = __dadd_rn(__dsub_rn(r[off], x0), __dmul_rn(h.beta, wa[m][n][e]));
+                }
+        }
+    }
+}
+
+inline size_t lowrank_smem(int64_t ldr, int NC) { return sizeof(double) * static_cast<size_t>(ldr) * (NC + 8); }
+
+}  // namespace kz

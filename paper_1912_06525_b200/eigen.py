@@ -1,0 +1,148 @@
+"""Eigen-of-A low-rank index: the north-star form of LRC-Katz.
+
+BASELINE.json's north star describes LRC-Katz as "a low-rank term from a
+precomputed index of top-r eigenpairs (U, Lambda) of the symmetric adjacency
+A, plus a Conjugate Gradient correction on (I - beta A) x = residual".  The
+reference's own LRC is the Schur-complement form (lrc.py / kz_lrc_*); this
+is the other one, not in the reference, so its parity is
+against the exact solution (tests/test_gpu_eigen.py).
+
+``EigenIndex(graph_index, rank)`` wraps a ``GraphIndex`` (same operator, same
+solve order, same ids) and adds, in that order:
+
+* U: the ``rank`` Ritz vectors of A of largest |eigenvalue| (``which="LM"``,
+  default; "LA" = largest algebraic) by the device Lanczos of build.py (K1
+  SpMMs with b = 1, full reorthogonalisation, basis in HBM).  Both ends of
+  the spectrum bound CG's rate on I - beta A: deflating the most negative
+  eigenvalues as well cuts R-MAT 22 from 7 to 5 CG iterations per batch
+  (largest algebraic alone: 6);
+* AU = A U: one K1 SpMM of the r-column block;
+* T = U'AU and W = (I - beta T)^-1 (r x r).
+
+A query's low-rank term is the Galerkin point of span(U),
+x0 = U W U' b with U' b = beta (AU)[q, :]' -- exact for any orthonormal U, so
+Ritz-vector accuracy only changes iteration counts -- and the CG correction
+runs from x0 with the exact residual r0 = b - x0 + beta (AU) W U' b; both
+products are the two tall-skinny fp64 DMMA GEMMs of ``lowrank_init_kernel``
+(one fused pass), then the reference's CG recurrence (solver.py:62-101) with
+the stop test ||r|| <= tol ||b||.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+
+from . import _lib
+from .index import GraphIndex
+
+
+class EigenIndex:
+    """GraphIndex + top-r eigen basis of A (solver_kind "eigen")."""
+
+    solver_kind = "eigen"
+
+    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM"):
+        from .build import lanczos_topk
+
+        if not isinstance(gi, GraphIndex):
+            raise TypeError("EigenIndex wraps a GraphIndex")
+        torch = _lib.torch_cuda()
+        lib = _lib.load()
+        self.gi = gi
+        self.alpha = gi.alpha
+        self.spectral_norm = gi.spectral_norm
+        self.id_map = gi.id_map
+        n = gi.n
+        rank = int(rank)
+        if not 1 <= rank <= min(n, 384):
+            raise ValueError(f"rank {rank} outside [1, min(n, 384)]")
+        t0 = time.perf_counter()
+        op = gi.operator()
+
+        def apply(v):
+            y = torch.empty_like(v)
+            op.spmm(v, y, b=1)
+            return y
+
+        rng = np.random.default_rng(seed)
+        lr = lanczos_topk(apply, rank, rng.standard_normal(n), max_iter=max_steps, tol=lanczos_tol, rng=rng,
+                          psd=False, which=which)
+        t_lanczos = time.perf_counter() - t0
+        r = int(lr.ell)
+        ldr = (r + 3) // 4 * 4
+        ut = torch.zeros((ldr, n), dtype=torch.float64, device="cuda")
+        ut[:r] = torch.as_tensor(np.ascontiguousarray(lr.vectors.T), device="cuda")
+        aut = torch.zeros_like(ut)
+        op.spmm(ut[:r].contiguous(), aut[:r], b=r, chunk=1)
+        t = ut[:r] @ aut[:r].T
+        t = 0.5 * (t + t.T)
+        w = torch.linalg.inv(torch.eye(r, dtype=torch.float64, device="cuda") - self.alpha * t)
+        self.u = ut.T.contiguous()      # n x ldr row-major
+        self.au = aut.T.contiguous()    # n x ldr row-major
+        self.w = w.contiguous()
+        self.ritz_values = lr.values.copy()
+        self.rank, self.ldr = r, ldr
+        del ut, aut
+        desc = _lib.KzEigenDesc()
+        desc.n, desc.r, desc.ldr = n, r, ldr
+        desc.beta = float(self.alpha)
+        desc.op = op.handle.value
+        desc.u, desc.au, desc.w = self.u.data_ptr(), self.au.data_ptr(), self.w.data_ptr()
+        h = ctypes.c_void_p()
+        _lib.check(lib.kz_eigen_create(ctypes.byref(desc), ctypes.byref(h)))
+        self._lib, self._handle = lib, h
+        torch.cuda.synchronize()
+        self.build_stats = {"rank": r, "lanczos_seconds": t_lanczos,
+                            "build_seconds": time.perf_counter() - t0,
+                            "ritz_top": [float(v) for v in lr.values[:4]]}
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.kz_eigen_destroy(h)
+            except Exception:
+                pass
+            self._handle = None
+
+    def eigen_handle(self):
+        return self._handle
+
+    # -- the GraphIndex surface (ids, operator, masks) ----------------------
+    @property
+    def n(self):
+        return self.gi.n
+
+    @property
+    def graph(self):
+        return self.gi.graph
+
+    def operator(self):
+        return self.gi.operator()
+
+    def mask_operator(self):
+        return self.gi.mask_operator()
+
+    def solve_positions(self, internal):
+        return self.gi.solve_positions(internal)
+
+    def start_vector_to_solve(self, x0):
+        return self.gi.start_vector_to_solve(x0)
+
+    def device_perm(self):
+        return self.gi.device_perm()
+
+    def internal_id(self, original):
+        return self.gi.internal_id(original)
+
+    def internal_ids(self, originals):
+        return self.gi.internal_ids(originals)
+
+    def adjacency_internal(self):
+        return self.gi.adjacency_internal()
+
+    def rhs_for_position(self, pos):
+        return self.gi.rhs_for_position(pos)

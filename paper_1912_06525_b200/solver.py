@@ -77,10 +77,12 @@ def _batches(b, n):
 
 
 def cg_solve_device(idx, positions, tol=1e-8, max_iter=None, start_seed=None, rhs=None,
-                    out=None, clamp=True, perm=True):
+                    out=None, clamp=True, perm=True, eigen=False):
     """Batched CG on the index operator.  Returns (scores[b][n] cuda fp64,
     kz reports, device ms).  Scores are scattered to internal order when the
-    index is permuted (perm=True)."""
+    index is permuted (perm=True).  eigen=True (an EigenIndex, query columns,
+    no seeded start) starts every column at the eigen-of-A Galerkin point
+    (kz_eigen_batch)."""
     torch = _lib.torch_cuda()
     lib = _lib.load()
     op = idx.operator()
@@ -119,9 +121,15 @@ def cg_solve_device(idx, positions, tol=1e-8, max_iter=None, start_seed=None, rh
         sub = (_lib.KzReport * nb).from_address(ctypes.addressof(reports) + s * ctypes.sizeof(_lib.KzReport))
         args.reports = ctypes.cast(sub, ctypes.POINTER(_lib.KzReport))
         args.device_ms = ctypes.pointer(ms)
-        wsb = lib.kz_cg_workspace_bytes(op.handle, nb)
-        ws = _lib.Workspace.get(torch, wsb, slot="cg")
-        rc = lib.kz_cg_batch(op.handle, ctypes.byref(args), _lib.ptr(ws), ws.numel(), st)
+        if eigen:
+            eh = idx.eigen_handle()
+            wsb = lib.kz_eigen_workspace_bytes(eh, nb)
+            ws = _lib.Workspace.get(torch, wsb, slot="cg")
+            rc = lib.kz_eigen_batch(eh, ctypes.byref(args), _lib.ptr(ws), ws.numel(), st)
+        else:
+            wsb = lib.kz_cg_workspace_bytes(op.handle, nb)
+            ws = _lib.Workspace.get(torch, wsb, slot="cg")
+            rc = lib.kz_cg_batch(op.handle, ctypes.byref(args), _lib.ptr(ws), ws.numel(), st)
         _lib.check(rc)
         total_ms += ms.value
     return out, reports, total_ms
@@ -161,10 +169,18 @@ def query_cg_baseline(idx, q, tol=1e-8, max_iter=None, start_seed=None):
 def query_batch(idx, qs, tol=1e-8, max_iter=None, start_seed=None, device=False):
     """query() for many queries in one device call.
 
-    KatzIndex: LRC-Katz Schur PCG (solver.py:194-207).  GraphIndex (no
-    factors): plain CG, the only solver such an index supports."""
+    KatzIndex: LRC-Katz Schur PCG (solver.py:194-207).  EigenIndex: the
+    eigen-of-A low-rank start + CG correction (north-star LRC; a seeded
+    start falls back to plain CG from that start).  GraphIndex (no factors):
+    plain CG, the only solver such an index supports."""
     qs = np.atleast_1d(np.asarray(qs, dtype=np.int64))
-    if getattr(idx, "solver_kind", "cg") != "lrc":
+    kind = getattr(idx, "solver_kind", "cg")
+    if kind == "eigen" and start_seed is None:
+        _, pos = _positions(idx, qs)
+        scores, reps, ms = cg_solve_device(idx, pos, tol=tol, max_iter=max_iter, eigen=True)
+        reports = _reports(reps, ms / 1e3)
+        return (scores, reports) if device else (scores.cpu().numpy(), reports)
+    if kind != "lrc":
         return query_cg_baseline_batch(idx, qs, tol, max_iter, start_seed, device)
     from .lrc import lrc_query_batch
 
