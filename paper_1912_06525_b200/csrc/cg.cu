@@ -164,6 +164,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     }
     if (eig) {
         // y = beta W (AU)[q,:]';  x = U y;  r = b - x + beta (AU) y
+        if (w.bpad > 65535) return fail(KZ_EARG, "eigen start: at most 65535 columns per call");
         const dim3 cgrid(static_cast<unsigned>((eig->ldr + 127) / 128), static_cast<unsigned>(w.bpad));
         KZ_DISPATCH_C(C, lowrank_coef_kernel<CC><<<cgrid, 128, 0, st>>>(*eig, w.qpos, b, w.y); ::kz::note_launch());
         KZ_LAUNCH_CHECK();

@@ -66,12 +66,14 @@ def _positions(idx, qs):
     return internal, idx.solve_positions(internal)
 
 
-# largest block (in doubles) one device call may allocate per solve vector
+# largest block (in doubles) one device call may allocate per solve vector,
+# and the most query columns one call takes
 _MAX_BLOCK_DOUBLES = 2_000_000_000
+_MAX_COLUMNS = 8192
 
 
 def _batches(b, n):
-    per = max(1, min(b, _MAX_BLOCK_DOUBLES // max(n, 1)))
+    per = max(1, min(b, _MAX_COLUMNS, _MAX_BLOCK_DOUBLES // max(n, 1)))
     for s in range(0, b, per):
         yield s, min(b, s + per)
 

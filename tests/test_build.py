@@ -212,3 +212,49 @@ def test_cfg1_device_built_index_matches_reference_queries(gpu):
         assert abs(reps[j].iterations - rec["lrc_iters"][j]) <= 1
         want = rec["lrc_scores"][j]
         assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
+
+
+# ---- R-MAT scale-16 proxy: the largest R-MAT the reference can build ----
+PROXY = os.path.join(GOLDEN, "proxy16_ref.npz")
+
+
+@pytest.fixture(scope="module")
+def proxy(kz):
+    if not os.path.exists(PROXY):
+        pytest.skip("proxy16_ref.npz absent (tests/golden/make_proxy16.py)")
+    from paper_1912_06525_b200.generators import config_graph
+
+    return config_graph("proxy16"), np.load(PROXY)
+
+
+def test_proxy16_partition_matches_reference(kz, proxy):
+    g, rec = proxy
+    assert g.n == int(rec["n"]) and g.nnz == int(rec["nnz"])
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        bp = kz.partition_vertex_separator(g)
+    assert bp.n1 == int(rec["n1"]) and bp.n2 == int(rec["n2"])
+    assert np.array_equal(bp.perm, rec["perm"])
+    assert np.array_equal(bp.part_boundaries, rec["part_boundaries"])
+
+
+@pytest.mark.gpu
+def test_proxy16_device_build_and_lrc_queries_match_reference(gpu, proxy):
+    """LRC at the R-MAT 16 proxy (SURVEY §8c pins cfg2/cfg4's LRC parts
+    here): the device build answers the reference's queries within the
+    parity bar of the reference's own build."""
+    g, rec = proxy
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        idx = gpu.build_index(g, alpha=float(rec["alpha"]), ell=64, seed=0, spectral_norm=float(rec["spectral_norm"]))
+    assert idx.n2 == int(rec["n2"])
+    assert np.allclose(idx.lr.values, rec["sigma"], rtol=0, atol=1e-9)
+    scores, reps = gpu.query_batch(idx, rec["queries"], tol=1e-8)
+    for j in range(len(rec["queries"])):
+        assert abs(reps[j].iterations - rec["lrc_iters"][j]) <= 1
+        want = rec["lrc_scores"][j]
+        assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
