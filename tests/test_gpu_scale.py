@@ -83,3 +83,31 @@ def test_rmat_scale_parity(kz, cfg, ncheck):
     scores2, reps2 = kz.query_cg_baseline_batch(idx, qs, tol=spec["tol"], device=True)
     assert [r.iterations for r in reps] == [r.iterations for r in reps2]
     assert bool((scores2 == scores).all())
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
+def test_rmat_scale_eigen_form(kz, cfg):
+    """The bench's headline solver (eigen-form LRC, rank from the config) at
+    full size: every column's true residual within ~tol ||b||, agreement
+    with plain CG within cond * tol (both solve to tol; cond <= 3 at
+    beta = 0.5/lambda), fewer iterations, bit-identical reruns."""
+    import torch
+
+    from paper_1912_06525_b200 import generators as G
+
+    spec = G.CONFIGS[cfg]
+    g = G.rmat_graph_fast(spec["scale"])
+    lam = kz.spectral_norm(g)
+    gi = kz.GraphIndex(g, 0.5 / lam, spectral_norm=lam)
+    ei = kz.EigenIndex(gi, spec["ell"])
+    qs = G.sample_queries(g.original_ids, spec["b"], seed=0)
+    s_e, r_e = kz.query_batch(ei, qs, tol=spec["tol"], device=True)
+    s_c, r_c = kz.query_cg_baseline_batch(gi, qs, tol=spec["tol"], device=True)
+    assert all(r.converged for r in r_e)
+    assert max(r.iterations for r in r_e) < max(r.iterations for r in r_c)
+    rel = _true_residual(kz, gi, qs, s_e)
+    assert np.all(rel <= 5 * spec["tol"]), rel.max()
+    diff = (torch.linalg.vector_norm(s_e - s_c, dim=1) / torch.linalg.vector_norm(s_c, dim=1)).cpu().numpy()
+    assert np.all(diff <= 3 * 2 * spec["tol"]), diff.max()
+    s_e2, _ = kz.query_batch(ei, qs, tol=spec["tol"], device=True)
+    assert torch.equal(s_e, s_e2)
