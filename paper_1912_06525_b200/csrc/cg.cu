@@ -126,7 +126,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nchunks, st));
     if (int rc = zero_spmm_counters(g, nchunks, w.sp, st)) return rc;
     const size_t blk_bytes = sizeof(double) * static_cast<size_t>(w.bpad) * n;
-    KZ_CUDA(cudaMemsetAsync(w.x, 0, blk_bytes, st));
+    if (!eig) KZ_CUDA(cudaMemsetAsync(w.x, 0, blk_bytes, st));  // the eigen start writes every x
 
     const unsigned sgrid = static_cast<unsigned>(nchunks) * nb;
     const unsigned tgrid = static_cast<unsigned>(std::min<int64_t>(
@@ -178,8 +178,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_DISPATCH_C(C, {                                                                                     \
             KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                          static_cast<int>(smem)));                                             \
-            lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, n * CC, j0,   \
-                                                                            w.bpad);                           \
+            lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, w.p, n * CC, \
+                                                                            j0, w.bpad);                       \
             ::kz::note_launch();                                                                               \
         });                                                                                                    \
     } while (0)
@@ -193,7 +193,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
     }
-    KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));
+    if (!eig) KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));  // p0 = r0
 
     const double work = static_cast<double>(g->nnz + n) * w.bpad;
     const int lag = work > 2e7 ? 1 : 3;

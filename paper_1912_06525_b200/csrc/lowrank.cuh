@@ -56,14 +56,14 @@ __device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double
 
 // For the NC = 8*NT columns j0 .. j0+NC-1 (the column group; columns >= jmax
 // are padding and are neither read nor written):
-//   x = U y ;  r = (r - x) + beta * (AU y)          (r holds b on entry)
+//   x = U y ;  r = p = (r - x) + beta * (AU y)      (r holds b on entry; p0 = r0)
 // y's group columns are staged in shared memory once per CTA ([ldr][NC+8],
 // bank padded); each warp owns 16 rows of a 128-row tile and streams its U
 // and AU fragments from HBM kLrAhead k-steps ahead.  Persistent over tiles.
 template <int C, int NT>
 __global__ void __launch_bounds__(32 * kLrWarps, 2)
     lowrank_init_kernel(kz_eigen h, const double* __restrict__ y, double* __restrict__ x, double* __restrict__ r,
-                        int64_t ldv, int j0, int jmax) {
+                        double* __restrict__ p, int64_t ldv, int j0, int jmax) {
     constexpr int NC = 8 * NT;
     constexpr int YLD = NC + 8;
     extern __shared__ __align__(16) double ys[];
@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(32 * kLrWarps, 2)
                     const size_t off = static_cast<size_t>(j / C) * ldv + static_cast<size_t>(row) * C + (j % C);
                     const double x0 = ua[m][n][e];
                     x[off] = x0;
-                    r[off] = __dadd_rn(__dsub_rn(r[off], x0), __dmul_rn(h.beta, wa[m][n][e]));
+                    const double r0 = __dadd_rn(__dsub_rn(r[off], x0), __dmul_rn(h.beta, wa[m][n][e]));
+                    r[off] = r0;
+                    p[off] = r0;
                 }
         }
     }
