@@ -30,7 +30,12 @@ struct SolveState {
     int32_t* chunk_xstamp = nullptr;  // [nchunks]
     int32_t* n_active = nullptr;      // [1]
     int32_t* err = nullptr;           // [1]
+    int32_t* iter_dev = nullptr;      // [1] iteration number for graph replay (NULL: host-passed)
 };
+
+// The iteration number a kernel of the solve loop works on: passed by the
+// host, or read from the device counter when the loop is a replayed graph.
+__device__ __forceinline__ int cur_iter(const SolveState& s, int iter) { return s.iter_dev ? *s.iter_dev : iter; }
 
 enum FinalizeMode : int {
     FIN_WRITE = 0,      // out[col] = v
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(kThreads)
     const double mine = block_col_reduce<C, VEC>(acc, sm);
     double total;
     if (chunk_last_reduce<C>(red, chunk, local, mine, sm, total))
-        finalize_chunk<C>(mode, s, out, chunk, iter, total);
+        finalize_chunk<C>(mode, s, out, chunk, cur_iter(s, iter), total);
 }
 
 // CG residual update (solver.py:88-90) fused with r.r:  r -= a*q for the
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(kThreads)
                      int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter) {
     constexpr int VEC = Cfg<C>::VEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
+    iter = cur_iter(s, iter);
     if (s.chunk_xstamp[chunk] != iter) return;
     r += static_cast<size_t>(chunk) * ldr;
     q += static_cast<size_t>(chunk) * ldq;
@@ -264,6 +270,7 @@ __global__ void __launch_bounds__(kThreads)
                       int iter) {
     constexpr int VEC = Cfg<C>::VEC;
     const int chunk = blockIdx.x / nb, local = blockIdx.x - chunk * nb;
+    iter = cur_iter(s, iter);
     if (s.chunk_xstamp[chunk] != iter) return;
     x += static_cast<size_t>(chunk) * ldx;
     p += static_cast<size_t>(chunk) * ldp;

@@ -66,6 +66,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     s.chunk_xstamp = cv.take<int32_t>(w.nchunks);
     s.n_active = cv.take<int32_t>(1);
     s.err = cv.take<int32_t>(1);
+    s.iter_dev = cv.take<int32_t>(1);
     w.qpos = cv.take<int64_t>(w.bpad);
     w.iperm = cv.take<int64_t>(g->rows);
     w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
@@ -100,7 +101,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     if (a->qpos && !a->rhs)
         for (int j = 0; j < b; ++j)
             if (a->qpos[j] < 0 || a->qpos[j] >= n) return fail(KZ_EARG, "query position out of range");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamScope scope(static_cast<cudaStream_t>(stream));
+    cudaStream_t st = scope.st;
 
     Carver cv(ws, ws_bytes);
     CgWork w;
@@ -220,6 +222,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         sa.hook.err = s.err;
         sa.hook.n_active = s.n_active;
         sa.hook.iter = k;
+        sa.hook.iter_dev = s.iter_dev;
         if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
         KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
@@ -228,7 +231,9 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         return KZ_OK;
     };
     int64_t ran = 0;
-    int rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
+    // small solves are launch-bound: replay one captured iteration per step
+    int rc = work <= kGraphWork && graphs_enabled() ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
+                                                    : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
     if (rc) return rc;
 
     if (a->perm) {

@@ -13,6 +13,7 @@ namespace kz {
 int fail(int code, const std::string& msg);  // records msg, returns code
 void clear_error();
 void note_launch();  // counts every kernel launch of the library (kz_launch_count)
+void add_launches(long long n);
 
 #define KZ_CUDA(call)                                                                   \
     do {                                                                                \

@@ -17,6 +17,7 @@ int fail(int code, const std::string& msg) {
 }
 void clear_error() { g_last_error.clear(); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 }  // namespace kz
 

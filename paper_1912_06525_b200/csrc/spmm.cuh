@@ -194,6 +194,7 @@ struct DotHook {
     int32_t* err = nullptr;
     int32_t* n_active = nullptr;
     int32_t iter = 0;
+    const int32_t* iter_dev = nullptr;  // device iteration number (graph replay); overrides iter
 };
 
 struct SpmmArgs {
@@ -263,7 +264,7 @@ __device__ __forceinline__ void apply_dot_hook(const DotHook& h, int col, double
             atomicSub(h.n_active, 1);
         } else {
             h.alpha[col] = h.rs[col] / v;
-            h.xstamp[col] = h.iter;
+            h.xstamp[col] = h.iter_dev ? *h.iter_dev : h.iter;
         }
     }
 }
@@ -457,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         __syncwarp();
         if (lane == 0) {
             a.ccnt[chunk] = 0;
-            if (a.hook.mode == 1 && a.hook.chunk_xstamp) a.hook.chunk_xstamp[chunk] = a.hook.iter;
+            if (a.hook.mode == 1 && a.hook.chunk_xstamp)
+                a.hook.chunk_xstamp[chunk] = a.hook.iter_dev ? *a.hook.iter_dev : a.hook.iter;
         }
     }
     // the last warp out re-arms the queue for the next launch

@@ -24,6 +24,8 @@ ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--queries", type=int, default=1024)
 ap.add_argument("--s", type=int, default=100)
 ap.add_argument("--check", type=int, default=1)
+ap.add_argument("--solver", default="cg", choices=["cg", "eigen"])
+ap.add_argument("--rank", type=int, default=64)
 a = ap.parse_args()
 
 t0 = time.time()
@@ -31,6 +33,11 @@ g, pos = G.sbm_split(n=a.n, seed=0)
 t_graph = time.time() - t0
 lam = kz.spectral_norm(g)
 idx = kz.GraphIndex(g, 0.5 / lam, spectral_norm=lam)
+t_index = 0.0
+if a.solver == "eigen":  # the anchor solves start from the eigen-form low-rank term
+    t0 = time.time()
+    idx = kz.EigenIndex(idx, a.rank)
+    t_index = time.time() - t0
 # queries: endpoints of held-out pairs (nodes with positive partners), seeded
 cand = np.unique(pos.ravel())
 qs = G.sample_queries(cand, min(a.queries, cand.size), seed=0)
@@ -44,7 +51,8 @@ for u, v in pos:
     partners.setdefault(int(u), set()).add(int(v))
     partners.setdefault(int(v), set()).add(int(u))
 rec = [len({c for c, _ in p.candidates} & partners[int(p.query)]) / len(partners[int(p.query)]) for p in preds]
-out = {"n": g.n, "nnz": g.nnz, "lambda": lam, "queries": len(qs), "s": a.s, "T": a.s + 1,
+out = {"solver": a.solver, "rank": a.rank if a.solver == "eigen" else None, "index_s": round(t_index, 2),
+       "n": g.n, "nnz": g.nnz, "lambda": lam, "queries": len(qs), "s": a.s, "T": a.s + 1,
        "seconds": round(dt, 2), "queries_per_s": round(len(qs) / dt, 1), "graph_build_s": round(t_graph, 1),
        "recall_at_s_mean": round(float(np.mean(rec)), 4)}
 if a.check:
