@@ -31,6 +31,9 @@
 // they are bit-identical to scipy's csr_matvec.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
+
 #include "common.cuh"
 
 namespace kz {
@@ -38,7 +41,7 @@ constexpr int kMedDeg = 32;      // rows with deg <= kMedDeg are "short"
 constexpr int kSegLen = 1024;    // rows with deg > kSegLen are split into segments
 constexpr int kGroupTasks = 8;   // max tasks a warp dequeues at once (one dot slot)
 constexpr double kGroupCost = 1024.0;  // max neighbour-equivalents per work unit
-constexpr int kSuperGroups = 256; // groups reduced together by their last finisher
+constexpr int kSuperGroups = 256; // max groups reduced together by their last finisher
 constexpr int kSpmmMinBlocks = 5;
 }  // namespace kz
 
@@ -206,7 +209,8 @@ struct SpmmArgs {
     const int32_t* __restrict__ long_seg0;
     int32_t ntasks, nlong, nseg;
     int32_t ngroups;    // task groups (kGroupTasks consecutive tasks) per chunk
-    int32_t nsuper;     // super groups (kSuperGroups groups) per chunk
+    int32_t nsuper;     // super groups per chunk
+    int32_t super_size; // groups per super group (spmm_super_size)
     int32_t nchunks;
     int32_t nwarps;     // warps of the (persistent) launch
     const double* Xg;
@@ -278,11 +282,16 @@ __device__ __forceinline__ double warp_fixed_sum(const double* part, int cnt, in
     const int c = lane % C, sub = lane / C;
     double s = 0.0;
     if (sub < LPC) {
+        // 8 independent loads per round: the reduction is a latency chain on
+        // the tail of the launch (and the whole cost for small operators)
         double a[4] = {0.0, 0.0, 0.0, 0.0};
         int q = sub;
-        for (; q + 3 * LPC < cnt; q += 4 * LPC) {
+        for (; q + 7 * LPC < cnt; q += 8 * LPC) {
+            double v[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) a[u] += __ldcg(part + static_cast<size_t>(q + u * LPC) * C + c);
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + static_cast<size_t>(q + u * LPC) * C + c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] += v[u] + v[u + 4];
         }
         for (; q < cnt; q += LPC) a[0] += __ldcg(part + static_cast<size_t>(q) * C + c);
         s = (a[0] + a[1]) + (a[2] + a[3]);
@@ -430,15 +439,15 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
             __threadfence();
         }
         __syncwarp();
-        const int sg = gl / kSuperGroups;
-        const int sg_groups = min(kSuperGroups, a.ngroups - sg * kSuperGroups);
+        const int sg = gl / a.super_size;
+        const int sg_groups = min(a.super_size, a.ngroups - sg * a.super_size);
         int last = 0;
         if (lane == 0)
             last = atomicAdd(a.scnt + static_cast<size_t>(chunk) * a.nsuper + sg, 1) == sg_groups - 1;
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) continue;
         __threadfence();
-        const double sv = warp_fixed_sum<C>(a.gslot + (static_cast<size_t>(chunk) * a.ngroups + sg * kSuperGroups) * C,
+        const double sv = warp_fixed_sum<C>(a.gslot + (static_cast<size_t>(chunk) * a.ngroups + sg * a.super_size) * C,
                                             sg_groups, lane);
         if (lane < C) {
             a.sslot[(static_cast<size_t>(chunk) * a.nsuper + sg) * C + lane] = sv;
@@ -481,7 +490,17 @@ struct SpmmScratch {
     int64_t nlong_cap = 0, nsuper_cap = 0;
 };
 
-inline int64_t spmm_supers(int64_t ngroups) { return (ngroups + kSuperGroups - 1) / kSuperGroups; }
+// Groups per super group: ~sqrt(ngroups) balances the two serial reductions
+// at the end of a chunk (super group, then chunk); small operators would
+// otherwise wait ~20 us on one warp summing 256 slots.
+inline int spmm_super_size(int64_t ngroups) {
+    int64_t s = static_cast<int64_t>(std::ceil(std::sqrt(static_cast<double>(std::max<int64_t>(ngroups, 1)))));
+    return static_cast<int>(std::min<int64_t>(kSuperGroups, std::max<int64_t>(16, s)));
+}
+inline int64_t spmm_supers(int64_t ngroups) {
+    const int64_t s = spmm_super_size(ngroups);
+    return (ngroups + s - 1) / s;
+}
 
 // sizes for the largest of several operators (LRC reuses one scratch)
 struct SpmmDims {
@@ -541,6 +560,7 @@ inline SpmmArgs make_spmm_args(const kz_graph* g, const SpmmScratch& s) {
     a.group_first = g->group_first;
     a.ngroups = g->ngroups;
     a.nsuper = static_cast<int32_t>(spmm_supers(g->ngroups));
+    a.super_size = spmm_super_size(g->ngroups);
     a.partial = s.partial;
     a.rowcnt = s.rowcnt;
     a.gslot = s.gslot;
