@@ -120,6 +120,7 @@ void carve_lrc(Carver& cv, const kz_lrc* h, int b, int C, LrcWork& w) {
     s.chunk_xstamp = cv.take<int32_t>(w.nch);
     s.n_active = cv.take<int32_t>(1);
     s.err = cv.take<int32_t>(1);
+    s.iter_dev = cv.take<int32_t>(1);
     w.qpos = cv.take<int64_t>(w.bpad);
     w.iperm = cv.take<int64_t>(n);
 }
@@ -323,7 +324,8 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
     if (!mode_pcg)
         for (int j = 0; j < b; ++j)
             if (a->qpos[j] < 0 || a->qpos[j] >= n) return fail(KZ_EARG, "query position out of range");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamScope scope(static_cast<cudaStream_t>(stream));
+    cudaStream_t st = scope.st;
     Carver cv(ws, ws_bytes);
     LrcWork w;
     carve_lrc(cv, h, b, C, w);
@@ -426,6 +428,7 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
             hk.err = s.err;
             hk.n_active = s.n_active;
             hk.iter = k;
+            hk.iter_dev = s.iter_dev;
             int r2;
             if ((r2 = cx.schur(w.p, l2, w.q, &hk, s.chunk_active))) return r2;
             const unsigned sg = static_cast<unsigned>(nch) * w.nb;
@@ -442,7 +445,11 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
             return KZ_OK;
         };
         int64_t ran = 0;
-        if ((rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran))) return rc;
+        // launch-bound small solves replay one captured PCG iteration per step
+        if ((rc = work * w.bpad <= kGraphWork && graphs_enabled()
+                      ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
+                      : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran)))
+            return rc;
     }
 
     if (!mode_pcg) {
