@@ -99,8 +99,12 @@ struct StreamScope {
 // solves with at most this much per-iteration work ((nnz + n) * columns)
 // replay a captured iteration graph (launch overhead dominates below it)
 constexpr double kGraphWork = 2e9;
+// Opt-in (KZ_GRAPHS=1): measured with tools/timeline.py, capture +
+// instantiate costs 0.2-1.2 ms per solve while the loop's launch gaps are
+// ~10 us per kernel, so at every BASELINE config the host-driven loop is as
+// fast or faster (R-MAT 18, 64 queries: 3.37 vs 4.55 ms span).
 inline bool graphs_enabled() {
-    static const bool on = std::getenv("KZ_NO_GRAPHS") == nullptr;
+    static const bool on = std::getenv("KZ_GRAPHS") != nullptr;
     return on;
 }
 

@@ -263,3 +263,30 @@ def test_operator_rejects_out_of_range_columns(torch, kz):
         kz.DeviceOperator(off, np.array([1, 2], dtype=np.int32), 2)  # column 2 of a 2-column operator
     with pytest.raises(ValueError):
         kz.DeviceOperator(off, np.array([1, -1], dtype=np.int32), 2)
+
+
+def test_graph_replayed_loops_match(kz):
+    """The opt-in CUDA-graph iteration loop (KZ_GRAPHS=1, driver.cuh) gives
+    the same CG and LRC answers as the host-driven loop."""
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys, numpy as np
+sys.path.insert(0, os.getcwd())
+import paper_1912_06525_b200 as kz
+idx = kz.load_index("tests/golden/ba300.klrc")
+rec = np.load("tests/golden/ba300.npz")
+q = rec["queries"]
+for fn, key in ((kz.query_cg_baseline_batch, "cg"), (kz.query_batch, "lrc")):
+    s, r = fn(idx, q, tol=1e-10)
+    for j in range(len(q)):
+        want = rec[f"{key}_1e-10_scores"][j]
+        assert np.linalg.norm(s[j] - want) <= 1e-10 * np.linalg.norm(want), (key, j)
+        assert abs(r[j].iterations - rec[f"{key}_1e-10_iters"][j]) <= 1
+print("graphs ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KZ_GRAPHS="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "graphs ok" in out.stdout, out.stderr[-2000:]
