@@ -138,16 +138,20 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     if (a->rhs) {
         KZ_DISPATCH_C(C, load_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.r, a->rhs, n, n * CC, b, nchunks); ::kz::note_launch());
     } else {
-        KZ_CUDA(cudaMemsetAsync(w.r, 0, blk_bytes, st));
         KZ_CUDA(cudaMemcpyAsync(w.qpos, a->qpos, sizeof(int64_t) * b, cudaMemcpyHostToDevice, st));
-        KZ_DISPATCH_C(C, scatter_rhs_kernel<CC><<<b, kThreads, 0, st>>>(w.r, n * CC, g->rowptr, g->colidx, w.qpos, b, a->beta); ::kz::note_launch());
+        if (!eig) {  // the eigen start writes r itself and adds the rhs afterwards
+            KZ_CUDA(cudaMemsetAsync(w.r, 0, blk_bytes, st));
+            KZ_DISPATCH_C(C, scatter_rhs_kernel<CC><<<b, kThreads, 0, st>>>(w.r, n * CC, g->rowptr, g->colidx, w.qpos, b, a->beta); ::kz::note_launch());
+        }
     }
     KZ_LAUNCH_CHECK();
     // ||b||, optional start vector (solver.py:51-59), init finalize
-    KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red,
-                                                                     (a->x0 || eig) ? FIN_INIT_B : FIN_INIT_BR,
-                                                                     s, nullptr, 0); ::kz::note_launch());
-    KZ_LAUNCH_CHECK();
+    if (!eig) {
+        KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red,
+                                                                         a->x0 ? FIN_INIT_B : FIN_INIT_BR,
+                                                                         s, nullptr, 0); ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
+    }
     if (a->x0) {
         KZ_DISPATCH_C(C, broadcast_kernel<CC><<<tgrid, kThreads, 0, st>>>(w.x, a->x0, n, n * CC, b, nchunks); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
@@ -192,6 +196,10 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
 #undef KZ_LR
             KZ_LAUNCH_CHECK();
         }
+        KZ_DISPATCH_C(C, eigen_add_rhs_kernel<CC><<<w.bpad, kThreads, 0, st>>>(w.r, w.p, n * CC, g->rowptr, g->colidx,
+                                                                                w.qpos, b, a->beta, s.bnorm2);
+                      ::kz::note_launch());
+        KZ_LAUNCH_CHECK();
         KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
     }

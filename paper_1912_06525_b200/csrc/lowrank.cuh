@@ -56,7 +56,8 @@ __device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double
 
 // For the NC = 8*NT columns j0 .. j0+NC-1 (the column group; columns >= jmax
 // are padding and are neither read nor written):
-//   x = U y ;  r = p = (r - x) + beta * (AU y)      (r holds b on entry; p0 = r0)
+//   x = U y ;  r = p = beta * (AU y) - x    (the rhs b = beta A e_q is added
+//   afterwards by eigen_add_rhs_kernel, so r is written, never read)
 // y's group columns are staged in shared memory once per CTA ([ldr][NC+8],
 // bank padded); each warp owns 16 rows of a 128-row tile and streams its U
 // and AU fragments from HBM kLrAhead k-steps ahead.  Persistent over tiles.
@@ -143,12 +144,34 @@ __global__ void __launch_bounds__(32 * kLrWarps, 2)
                     const size_t off = static_cast<size_t>(j / C) * ldv + static_cast<size_t>(row) * C + (j % C);
                     const double x0 = ua[m][n][e];
                     x[off] = x0;
-                    const double r0 = __dadd_rn(__dsub_rn(r[off], x0), __dmul_rn(h.beta, wa[m][n][e]));
+                    const double r0 = __dsub_rn(__dmul_rn(h.beta, wa[m][n][e]), x0);
                     r[off] = r0;
                     p[off] = r0;
                 }
         }
     }
+}
+
+// r, p (chunked) += beta at the neighbours of q_j: the rhs b = beta A e_q
+// (index.py:93-101) added onto r0 = beta (AU) y - x0; and ||b||^2 =
+// beta^2 deg(q_j) for the stop threshold (solver.py:71-72).
+template <int C>
+__global__ void eigen_add_rhs_kernel(double* __restrict__ r, double* __restrict__ p, int64_t ld,
+                                     const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+                                     const int64_t* __restrict__ qpos, int b, double beta, double* __restrict__ bnorm2) {
+    const int j = blockIdx.x;
+    if (j >= b) {
+        if (threadIdx.x == 0) bnorm2[j] = 0.0;
+        return;
+    }
+    const int64_t q = qpos[j];
+    const int beg = rowptr[q], end = rowptr[q + 1];
+    for (int k = beg + threadIdx.x; k < end; k += blockDim.x) {
+        const size_t off = static_cast<size_t>(j / C) * ld + static_cast<size_t>(colidx[k]) * C + (j % C);
+        r[off] = __dadd_rn(r[off], beta);
+        p[off] = __dadd_rn(p[off], beta);
+    }
+    if (threadIdx.x == 0) bnorm2[j] = __dmul_rn(__dmul_rn(beta, beta), static_cast<double>(end - beg));
 }
 
 inline size_t lowrank_smem(int64_t ldr, int NC) { return sizeof(double) * static_cast<size_t>(ldr) * (NC + 8); }
