@@ -105,3 +105,21 @@ def test_eigen_rejects_seeded_rhs_forms(env):
     assert np.array_equal(s1, s2)
     with pytest.raises(ValueError):
         kz.EigenIndex(gi, 0)
+
+
+@pytest.mark.parametrize("edges,rank", [([(0, 1), (1, 2), (0, 2)], 3), ([(0, 1), (1, 2), (2, 3), (3, 4)], 5),
+                                        ([(0, 1)], 1), ([(0, i) for i in range(1, 7)], 4)])
+def test_eigen_tiny_graphs_full_rank(env, edges, rank):
+    """Ranks up to n (ldr padding beyond n rows), against the exact solve."""
+    kz = env[0]
+    g = kz.from_edges(edges)
+    a = g.adjacency().astype(np.float64).tocsc()
+    lmax = float(np.max(np.linalg.eigvalsh(a.toarray())))
+    alpha = 0.5 / lmax
+    gi = kz.GraphIndex(g, alpha=alpha, spectral_norm=lmax)
+    ei = kz.EigenIndex(gi, rank)
+    scores, reps = kz.query_batch(ei, g.original_ids, tol=1e-12)
+    want = exact(a, alpha, np.arange(g.n))
+    for j in range(g.n):
+        assert np.linalg.norm(scores[j] - want[j]) <= 1e-10 * np.linalg.norm(want[j])
+        assert reps[j].converged
