@@ -44,7 +44,19 @@ struct DenseArgs {
     int64_t rows_tile;  // output rows per CTA tile (256 * TM)
     double* part;  // [mtiles][ksplit][threads][TM*NC]
     int32_t* cnt;  // [mtiles]
+    const int32_t* chunk_active;  // optional flags of this launch's chunks (all 0: nothing to do)
+    int nchunk;                   // chunks covered by this launch
 };
+
+// A launch whose chunks are all inactive (columns frozen by the PCG masks)
+// returns at once; the decision is uniform over the grid, so no CTA of a
+// split-K launch touches the tile counters.
+__device__ __forceinline__ bool dense_skip(const DenseArgs& a) {
+    if (!a.chunk_active) return false;
+    for (int c = 0; c < a.nchunk; ++c)
+        if (a.chunk_active[c]) return false;
+    return true;
+}
 
 __device__ __forceinline__ bool dense_tile_empty(const DenseArgs& a, int64_t i0, int64_t k0, int64_t k1) {
     if (k0 >= k1) return true;
@@ -59,6 +71,7 @@ __device__ __forceinline__ bool dense_tile_empty(const DenseArgs& a, int64_t i0,
 // shared memory in 16-byte pieces, i.e. 2*TM FMAs per shared load.
 template <int C, int NCH, int TM>
 __global__ void __launch_bounds__(kDenseThreads, (TM * C * NCH <= 16) ? 2 : 1) dense_kernel(DenseArgs a) {
+    if (dense_skip(a)) return;
     constexpr int NC = C * NCH;
     constexpr int ROWS = kDenseThreads * TM;
     static_assert(NC % 2 == 0 || NC == 1, "column count");
@@ -231,6 +244,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 template <int C, int NT>
 __global__ void __launch_bounds__(32 * kDmmaWarps) dense_dmma_kernel(DenseArgs a) {
+    if (dense_skip(a)) return;
     constexpr int NC = 8 * NT;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int mt = blockIdx.x / a.ksplit, ks = blockIdx.x - mt * a.ksplit;
@@ -358,6 +372,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 template <int C, int NT>
 __global__ void __launch_bounds__(32 * kDmmaWarps, 2) dense_dmma2_kernel(DenseArgs a) {
+    if (dense_skip(a)) return;
     constexpr int NC = 8 * NT;
     extern __shared__ __align__(16) double d2s[];
     double* As = d2s;                       // [2][KS][ALd]
@@ -515,7 +530,7 @@ inline size_t dense_part_doubles(int64_t M, int64_t K, int NC) {
 // A zero-padded up to lda columns (16-byte aligned pair loads).
 inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int tri, const double* X,
                         int64_t ldx, double* Y, int64_t ldy, double alpha, double beta, int C, int nch,
-                        const DenseScratch& ds, cudaStream_t st) {
+                        const DenseScratch& ds, cudaStream_t st, const int32_t* chunk_active = nullptr) {
     if (M == 0) return KZ_OK;
     if (lda % 2 != 0 || lda < M + (M & 1)) return fail(KZ_EARG, "dense operand needs an even, padded lda");
     auto group = [&](int left) {
@@ -548,6 +563,8 @@ inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int 
             a.kper = kper;
             a.part = ds.part;
             a.cnt = ds.cnt;
+            a.chunk_active = chunk_active ? chunk_active + c0 : nullptr;
+            a.nchunk = g;
             if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * kD2Rows * g * C > ds.part_cap ||
                                mtiles > ds.cnt_cap))
                 return fail(KZ_EARG, "dense scratch too small");
@@ -597,6 +614,8 @@ inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int 
             a.kper = kper;
             a.part = ds.part;
             a.cnt = ds.cnt;
+            a.chunk_active = chunk_active ? chunk_active + c0 : nullptr;
+            a.nchunk = g;
             if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * kDmmaRows * g * C > ds.part_cap ||
                                mtiles > ds.cnt_cap))
                 return fail(KZ_EARG, "dense scratch too small");
@@ -638,6 +657,8 @@ inline int launch_dense(const double* A, int64_t lda, int64_t M, int64_t K, int 
         a.kper = kper;
         a.part = ds.part;
         a.cnt = ds.cnt;
+        a.chunk_active = chunk_active ? chunk_active + c0 : nullptr;
+        a.nchunk = g;
         if (ksplit > 1 && (static_cast<size_t>(mtiles) * ksplit * a.rows_tile * g * C > ds.part_cap ||
                            mtiles > ds.cnt_cap))
             return fail(KZ_EARG, "dense scratch too small");

@@ -231,20 +231,21 @@ struct LrcCtx {
     }
 
     // z = L^-T (I + U D U') L^-1 r
-    int precond(const double* r, int64_t ldr, double* z, int64_t ldz) {
+    // chunk_active (optional): skip column groups whose columns have all stopped
+    int precond(const double* r, int64_t ldr, double* z, int64_t ldz, const int32_t* chunk_active = nullptr) {
         const int64_t n2 = h->n2, ell = h->ell;
         int rc;
-        if ((rc = launch_dense(h->linvT, h->ld2, n2, n2, 2, r, ldr, w->t2, n2 * C, 1.0, 0.0, C, nch, w->ds, st)))
+        if ((rc = launch_dense(h->linvT, h->ld2, n2, n2, 2, r, ldr, w->t2, n2 * C, 1.0, 0.0, C, nch, w->ds, st, chunk_active)))
             return rc;
         if (ell > 0) {
             if ((rc = launch_dense(h->u, h->ldl, ell, n2, 0, w->t2, n2 * C, w->cl, ell * C, 1.0, 0.0, C, nch, w->ds,
-                                   st)))
+                                   st, chunk_active)))
                 return rc;
             if ((rc = launch_dense(h->udT, h->ld2, n2, ell, 0, w->cl, ell * C, w->t2, n2 * C, 1.0, 1.0, C, nch,
-                                   w->ds, st)))
+                                   w->ds, st, chunk_active)))
                 return rc;
         }
-        return launch_dense(h->linv, h->ld2, n2, n2, 1, w->t2, n2 * C, z, ldz, 1.0, 0.0, C, nch, w->ds, st);
+        return launch_dense(h->linv, h->ld2, n2, n2, 1, w->t2, n2 * C, z, ldz, 1.0, 0.0, C, nch, w->ds, st, chunk_active);
     }
 
     int coldot(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t rows, int mode,
@@ -436,7 +437,7 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
                                                                             FIN_PCG_RR, s, k);
                           note_launch());
             KZ_LAUNCH_CHECK();
-            if ((r2 = cx.precond(w.r, l2, w.z, l2))) return r2;
+            if ((r2 = cx.precond(w.r, l2, w.z, l2, s.chunk_active))) return r2;
             if ((r2 = cx.coldot(w.r, l2, w.z, l2, n2, FIN_PCG_RZ, nullptr, k))) return r2;
             KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sg, kThreads, 0, st>>>(xk, w.p, w.z, n2, ldxk, l2, l2, w.nb,
                                                                              s, k);
