@@ -49,15 +49,20 @@ def initial_state(b, start_seed, apply_a):
     return x, b - apply_a(x)
 
 
-def cg(apply_a, b, tol=1e-8, max_iter=None, start_seed=None):
-    """solver.py:62-101"""
+def cg(apply_a, b, tol=1e-8, max_iter=None, start_seed=None, x0=None):
+    """solver.py:62-101; x0 (not in the reference) replaces the seeded start
+    of _initial_state (solver.py:51-59) by a given vector."""
     b = np.asarray(b, dtype=np.float64)
     n = b.size
     if max_iter is None:
         max_iter = 10 * n
     t0 = time.perf_counter()
     thresh = tol * np.linalg.norm(b)
-    x, r = initial_state(b, start_seed, apply_a)
+    if x0 is not None:
+        x = np.array(x0, dtype=np.float64)
+        r = b - apply_a(x)
+    else:
+        x, r = initial_state(b, start_seed, apply_a)
     rnorm = np.linalg.norm(r)
     it = 0
     if rnorm > thresh:
@@ -99,6 +104,28 @@ def query_cg_csr(a, beta, q, tol=1e-8, max_iter=None, start_seed=None):
     rhs = np.zeros(n)
     rhs[a.indices[a.indptr[q] : a.indptr[q + 1]]] = beta
     x, rep = cg(lambda v: v - beta * (a @ v), rhs, tol, max_iter, start_seed)
+    return np.maximum(x, 0.0), rep
+
+
+# ---------------------------------------------------------------------------
+# Eigen-form LRC (the north star's "low-rank term from a
+# top-r eigen index of A plus a CG correction", not in the reference): the
+# start is the Galerkin point x0 = U W U'b of the index basis (U'b = beta
+# (AU)[q,:] for b = beta A e_q), then the reference's cg recurrence from x0
+# with r0 = b - M x0 formed by the operator (the device forms it from AU;
+# the two agree to roundoff).  U, AU (n x r, internal order) and W come from
+# the device index (EigenIndex.basis_internal).
+# ---------------------------------------------------------------------------
+
+
+def query_eigen_csr(a, beta, q, u, au, w, tol=1e-8, max_iter=None):
+    """Scores (clamped) and report of one query, eigen-form start + cg."""
+    n = a.shape[0]
+    rhs = np.zeros(n)
+    rhs[a.indices[a.indptr[q] : a.indptr[q + 1]]] = beta
+    y = beta * (w @ au[q])
+    x0 = u @ y
+    x, rep = cg(lambda v: v - beta * (a @ v), rhs, tol, max_iter, x0=x0)
     return np.maximum(x, 0.0), rep
 
 

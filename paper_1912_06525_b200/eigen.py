@@ -111,6 +111,17 @@ class EigenIndex:
     def eigen_handle(self):
         return self._handle
 
+    def basis_internal(self):
+        """(U, AU, W) as host arrays with rows in internal node order (U and
+        AU live in the GraphIndex's solve order on the device)."""
+        r = self.rank
+        u = self.u[:, :r].cpu().numpy()
+        au = self.au[:, :r].cpu().numpy()
+        inv = getattr(self.gi, "_inv", None) if getattr(self.gi, "_order", None) is not None else None
+        if inv is not None:
+            u, au = u[inv], au[inv]
+        return u, au, self.w.cpu().numpy()
+
     # -- the GraphIndex surface (ids, operator, masks) ----------------------
     @property
     def n(self):

@@ -123,3 +123,25 @@ def test_eigen_tiny_graphs_full_rank(env, edges, rank):
     for j in range(g.n):
         assert np.linalg.norm(scores[j] - want[j]) <= 1e-10 * np.linalg.norm(want[j])
         assert reps[j].converged
+
+
+@pytest.mark.parametrize("reorder", [None, "rcm"])
+def test_eigen_matches_cpu_oracle_of_the_same_algorithm(env, reorder):
+    """GPU eigen-form LRC against its CPU restatement (oracle.query_eigen_csr:
+    the same basis, the reference's cg recurrence from the same start):
+    rel L2 <= 1e-10 per column and iterations +/-1 -- the BASELINE parity bar
+    applied to the headline solver."""
+    from oracle import katz_oracle as O
+
+    kz, g, a, lmax, _ = env
+    alpha = 0.5 / lmax
+    gi = kz.GraphIndex(g, alpha=alpha, spectral_norm=lmax, reorder=reorder)
+    ei = kz.EigenIndex(gi, 16)
+    u, au, w = ei.basis_internal()
+    qs = g.original_ids[np.linspace(0, g.n - 1, 12).astype(int)]
+    for tol in (1e-8, 1e-10):
+        scores, reps = kz.query_batch(ei, qs, tol=tol)
+        for j, q in enumerate(qs):
+            want, orep = O.query_eigen_csr(a.tocsr(), alpha, int(np.searchsorted(g.original_ids, q)), u, au, w, tol=tol)
+            assert abs(reps[j].iterations - orep.iterations) <= 1, (j, reps[j].iterations, orep.iterations)
+            assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
