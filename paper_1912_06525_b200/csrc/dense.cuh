@@ -12,9 +12,15 @@
 //   t += (U D) c    A = (U D)^T (ell x n2)              (factor.py:336-337)
 // Tiles entirely outside the triangle are skipped.  The K range is split
 // over CTAs (enough to cover 148 SMs when M is small); the last CTA of a row
-// tile reduces the split partials in a fixed order (deterministic).  fp64
-// has no tcgen05 kind on sm_100a and the DMMA rate equals the CUDA-core
-// DFMA rate on B200, so this is a bandwidth-first CUDA-core kernel.
+// tile reduces the split partials in a fixed order (deterministic).
+//
+// Three kernels share this contract: dense_kernel (CUDA-core FMA, for column
+// groups that are not a multiple of 8), dense_dmma_kernel (fp64 tensor cores,
+// mma.sync.m8n8k4.f64, fragments straight from global memory: small and
+// mid-size operators) and dense_dmma2_kernel (shared-memory staged A/X slabs
+// by cp.async: n2 >= 8192).  tcgen05 has no fp64 kind on sm_100a, so DMMA is
+// the fp64 tensor path; its measured ceiling here is the cuBLAS DGEMM rate,
+// 35.5 TFLOP/s (profiles/r01_fp64_peak.json).
 #pragma once
 
 #include "spmm.cuh"
