@@ -14,6 +14,14 @@ scope.
 """
 
 from .eigen import EigenIndex
+from .factor_ops import (
+    apply_approx_schur_inverse,
+    apply_correction,
+    block_cholesky,
+    build_blocks,
+    check_partition,
+    dense_cholesky,
+)
 from .build import (
     DisconnectedGraphError,
     PartitionConfig,
@@ -45,8 +53,11 @@ from .graph import (
     InadmissibleAlphaError,
     KatzParams,
     from_edges,
+    from_edges_device,
     hardest_alpha,
     largest_connected_component,
+    largest_connected_component_device,
+    load_edge_list,
     spectral_norm,
 )
 from .index import (

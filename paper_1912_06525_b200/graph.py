@@ -11,6 +11,7 @@ indices, no stored values) for the sm_100a kernels.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -19,7 +20,13 @@ from . import _lib
 
 
 class GraphParseError(ValueError):
-    """Malformed edge-list input (graph.py:17-24)."""
+    """Malformed edge-list input; carries the 1-based line number (graph.py:17-24)."""
+
+    def __init__(self, message, line_no=None):
+        if line_no is not None:
+            message = f"line {line_no}: {message}"
+        super().__init__(message)
+        self.line_no = line_no
 
 
 class ConvergenceError(RuntimeError):
@@ -154,6 +161,55 @@ def largest_connected_component(g):
     cols = remap[g.col_indices[mask]]
     return Graph(n=int(keep.size), row_offsets=offsets, col_indices=cols,
                  original_ids=g.original_ids[keep].copy())
+
+
+def load_edge_list(source, fmt="auto"):
+    """Read an undirected edge list into a Graph (graph.py:157-208).
+
+    source: path, bytes or file-like; one edge per line, two non-negative
+    integer ids separated by whitespace or a comma ("auto": a line holding a
+    comma is CSV); blank lines and '#' comments are skipped.  Ids are
+    compacted to 0..n-1 in increasing order and kept as original_ids;
+    duplicates and self loops are dropped.  GraphParseError (with the line
+    number) on a malformed line or when no edge remains.  Parsing is host
+    text processing; the CSR is then built like from_edges.
+    """
+    if fmt not in ("auto", "whitespace", "csv"):
+        raise ValueError(f"unknown format {fmt!r}")
+    if isinstance(source, (str, os.PathLike)):
+        with open(source, "rb") as fh:
+            data = fh.read()
+    elif isinstance(source, bytes):
+        data = source
+    else:
+        data = source.read()
+        if isinstance(data, str):
+            data = data.encode()
+    us, vs = [], []
+    for line_no, raw in enumerate(data.decode("utf-8", errors="replace").splitlines(), 1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        if fmt == "csv" or (fmt == "auto" and "," in line):
+            toks = [t.strip() for t in line.split(",") if t.strip()]
+        else:
+            toks = line.split()
+        if len(toks) != 2:
+            raise GraphParseError(f"expected 2 fields, got {len(toks)}", line_no)
+        try:
+            u, v = int(toks[0]), int(toks[1])
+        except ValueError:
+            raise GraphParseError(f"non-integer node id in {toks!r}", line_no) from None
+        if u < 0 or v < 0:
+            raise GraphParseError("negative node id", line_no)
+        if u != v:
+            us.append(u)
+            vs.append(v)
+    if not us:
+        raise GraphParseError("no edges in input")
+    arr = np.stack([np.asarray(us, dtype=np.int64), np.asarray(vs, dtype=np.int64)], axis=1)
+    ids = np.unique(arr)
+    return from_edges(np.searchsorted(ids, arr), n=ids.size, original_ids=ids)
 
 
 def from_edges_device(u, v, n, original_ids=None):

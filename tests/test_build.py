@@ -258,3 +258,73 @@ def test_proxy16_device_build_and_lrc_queries_match_reference(gpu, proxy):
         assert abs(reps[j].iterations - rec["lrc_iters"][j]) <= 1
         want = rec["lrc_scores"][j]
         assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
+
+
+# ---- the reference's partition/factor helpers under their own names ----
+@pytest.mark.parametrize("name", ["er60", "ba300", "recall"])
+def test_build_blocks_check_partition_block_cholesky(kz, name):
+    """build_blocks / check_partition / block_cholesky (partition.py:250-297,
+    factor.py:127-152) reproduce the reference's M12 and part factors."""
+    ref = ref_index(kz, name)
+    g = graph_of(kz, ref)
+    m11, m12, m22 = kz.build_blocks(g, ref.alpha, ref.bp)
+    assert np.array_equal(m12.indptr, ref.m12.indptr) and np.array_equal(m12.indices, ref.m12.indices)
+    assert m12.data.tobytes() == ref.m12.data.tobytes()
+    assert m11.shape == (ref.n1, ref.n1) and m22.shape == (ref.n2, ref.n2)
+    assert np.allclose(m22.diagonal(), 1.0)
+    assert kz.check_partition(g, ref.bp)
+    bad = kz.BlockPartition(perm=ref.bp.perm[::-1].copy(), inv_perm=np.argsort(ref.bp.perm[::-1]),
+                            part_boundaries=ref.bp.part_boundaries, n1=ref.n1, n2=ref.n2)
+    assert not kz.check_partition(g, bad)
+    bc = kz.block_cholesky(m11, ref.bp.part_boundaries)
+    for b in range(bc.num_blocks):
+        assert np.array_equal(bc.orders[b], ref.bc.orders[b])
+        assert bc.factors[b].data.tobytes() == ref.bc.factors[b].data.tobytes()
+    with pytest.raises(kz.InadmissibleAlphaError):
+        kz.build_blocks(g, -0.1, ref.bp)
+
+
+def test_block_cholesky_names_the_failing_part(kz):
+    import scipy.sparse as sp
+
+    m11 = sp.csr_matrix(np.array([[1.0, 0, 0], [0, 1.0, 2.0], [0, 2.0, 1.0]]))
+    with pytest.raises(kz.FactorizationError, match="part 1"):
+        kz.block_cholesky(m11, [0, 1, 3])
+
+
+def test_load_edge_list_rules(kz):
+    g = kz.load_edge_list(b"# comment\n10 20\n20,30\n\n30 10\n10 10\n20 10\n")
+    assert g.n == 3 and list(g.original_ids) == [10, 20, 30] and g.num_edges == 3
+    for bad, line in ((b"1 2 3\n", 1), (b"1 2\nx 3\n", 2), (b"1 -2\n", 1)):
+        with pytest.raises(kz.GraphParseError) as err:
+            kz.load_edge_list(bad)
+        assert err.value.line_no == line
+    with pytest.raises(kz.GraphParseError):
+        kz.load_edge_list(b"5 5\n")
+    g2 = kz.load_edge_list(io.BytesIO(b"1\t2\n2 3\n"), fmt="whitespace")
+    assert g2.num_edges == 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["er60", "ba300"])
+def test_device_factor_helpers_match_oracle(gpu, name):
+    from oracle import katz_oracle as O
+
+    ref = ref_index(gpu, name)
+    ix = O.read_klrc(os.path.join(GOLDEN, f"{name}.klrc"))
+    g = graph_of(gpu, ref)
+    m11, m12, m22 = gpu.build_blocks(g, ref.alpha, ref.bp)
+    dc = gpu.dense_cholesky(m22)
+    assert np.linalg.norm(dc.factor - ref.dc.factor) <= 1e-12 * np.linalg.norm(ref.dc.factor)
+    rng = np.random.default_rng(1)
+    r = rng.standard_normal(ref.n2)
+    want = O.apply_approx_schur_inverse(ix, r)
+    got = gpu.apply_approx_schur_inverse(ref.dc, ref.lr, r)
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+    # R v against the dense restatement of factor.py:196-202
+    v = rng.standard_normal(ref.n2)
+    li = np.linalg.inv(ref.dc.factor)
+    dense_m11 = m11.toarray()
+    rv = li @ (m12.T @ np.linalg.solve(dense_m11, m12 @ (li.T @ v)))
+    got = gpu.apply_correction(ref.dc, ref.m12, ref.bc, v)
+    assert np.linalg.norm(got - rv) <= 1e-11 * max(1.0, np.linalg.norm(rv))
