@@ -1,6 +1,8 @@
 // graph.cu -- operator handles (kz_graph) and the K1 SpMM entry point.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -46,6 +48,7 @@ void free_graph(kz_graph* g) {
     cudaFree(g->tasks);
     cudaFree(g->group_first);
     cudaFree(g->long_seg0);
+    cudaFree(g->seg_range);
     delete g;
 }
 
@@ -57,9 +60,25 @@ __global__ void check_cols_kernel(const int32_t* __restrict__ col, int64_t nnz, 
     }
 }
 
-// Host schedule for K1 (see spmm.cuh): warp tasks in row order.
-void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<int4>& tasks,
-                    std::vector<int32_t>& long_seg0, std::vector<int32_t>& group_first, int32_t& max_deg) {
+// Column blocking of the long rows (see spmm.cuh).  For an operator whose
+// gathered chunk (cols * 32 doubles) is far larger than L2, rows of degree >
+// min_deg are cut by column block as well as by length, and those segments
+// run block-major: while block k's segments run, the gathered slice of X is
+// about slice_mb and stays L2-resident, so each of its rows is fetched from
+// HBM about once per chunk instead of about once per gather.
+struct SchedOpts {
+    int nblocks = 1;             // 1: no column blocking (long rows = deg > kSegLen)
+    int64_t min_deg = kSegLen;   // blocked: rows with deg > min_deg are long rows
+    int interleave = 1;          // blocked: short-row tasks spread over the block phases
+};
+
+// Host schedule for K1 (see spmm.cuh): warp tasks in row order, then (column
+// blocking) the long rows' segments block by block.  col is the host copy of
+// the column indices; with nblocks > 1 each long row's entries are stably
+// grouped by column block in place (this changes summation order only).
+void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, int32_t* col,
+                    const SchedOpts& o, std::vector<int4>& tasks, std::vector<int32_t>& long_seg0,
+                    std::vector<int2>& seg_range, std::vector<int32_t>& group_first, int32_t& max_deg) {
     std::vector<double> cost;
     int64_t s_open = -1, s_rows = 0;
     double s_cost = 0.0;
@@ -70,6 +89,8 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<in
             s_open = -1;
         }
     };
+    const bool blocked = o.nblocks > 1 && col != nullptr && cols > 0;
+    const int64_t min_deg = blocked ? std::min<int64_t>(std::max<int64_t>(o.min_deg, kMedDeg), kSegLen) : kSegLen;
     int32_t nlong = 0, nseg = 0;
     max_deg = 0;
     // granularity: aim for >= ~2 work units per resident warp of one chunk pass
@@ -77,6 +98,7 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<in
     const double unit = std::max(64.0, std::min(kGroupCost, est_total / (2.0 * kNumSMs * kSpmmMinBlocks * kWarps)));
     const int s_rows_max = unit >= 512.0 ? 32 : (unit >= 128.0 ? 8 : 4);
     const double s_cost_max = std::min(256.0, unit);
+    std::vector<int64_t> long_rows;  // blocked: rows deferred to the block phases
     for (int64_t i = 0; i < rows; ++i) {
         const int64_t d = rp[i + 1] - rp[i];
         max_deg = std::max<int32_t>(max_deg, static_cast<int32_t>(d));
@@ -89,24 +111,89 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, std::vector<in
             }
             s_rows += 1;
             s_cost += d + 4.0;
-        } else if (d <= kSegLen) {
+        } else if (d <= min_deg) {
             close_s(i);
             tasks.push_back(make_int4(static_cast<int>(i), 0, TASK_M, 0));
             cost.push_back(d + 8.0);
+        } else if (blocked) {
+            close_s(i);
+            long_rows.push_back(i);
         } else {
             close_s(i);
-            const int64_t ns = (d + kSegLen - 1) / kSegLen;
             long_seg0.push_back(nseg);
-            for (int64_t k = 0; k < ns; ++k) {
-                tasks.push_back(make_int4(static_cast<int>(i), nlong, TASK_L, static_cast<int>(k)));
-                cost.push_back(std::min<double>(kSegLen, d - k * kSegLen) + 8.0);
+            int k = 0;
+            for (int64_t p = rp[i]; p < rp[i + 1]; p += kSegLen, ++k) {
+                const int64_t e = std::min<int64_t>(p + kSegLen, rp[i + 1]);
+                tasks.push_back(make_int4(static_cast<int>(i), nlong, TASK_L, k));
+                cost.push_back(static_cast<double>(e - p) + 8.0);
+                seg_range.push_back(make_int2(static_cast<int>(p), static_cast<int>(e)));
             }
-            nseg += static_cast<int32_t>(ns);
+            nseg += k;
             ++nlong;
         }
     }
     close_s(rows);
-    long_seg0.push_back(nseg);
+    if (blocked) {
+        // group each long row's entries by column block (stable counting
+        // sort), then emit the segments block-major; a row's segments are
+        // numbered in queue order, so its last segment (the combiner) is
+        // dequeued last
+        const int K = o.nblocks;
+        const size_t nl = long_rows.size();
+        std::vector<int64_t> bstart(nl * (K + 1));
+        std::vector<int32_t> tmp;
+        std::vector<int64_t> cnt(K + 1);
+        auto block_of = [&](int32_t c) { return static_cast<int>((static_cast<int64_t>(c) * K) / cols); };
+        for (size_t l = 0; l < nl; ++l) {
+            const int64_t i = long_rows[l], b0 = rp[i], d = rp[i + 1] - b0;
+            std::fill(cnt.begin(), cnt.end(), 0);
+            for (int64_t p = 0; p < d; ++p) cnt[1 + block_of(col[b0 + p])] += 1;
+            for (int k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
+            for (int k = 0; k <= K; ++k) bstart[l * (K + 1) + k] = b0 + cnt[k];
+            tmp.resize(d);
+            for (int64_t p = 0; p < d; ++p) {
+                const int32_t c = col[b0 + p];
+                tmp[cnt[block_of(c)]++] = c;
+            }
+            std::copy(tmp.begin(), tmp.end(), col + b0);
+        }
+        std::vector<int32_t> seg0(nl + 1, 0), next(nl, 0);
+        for (size_t l = 0; l < nl; ++l) {
+            int64_t ns = 0;
+            for (int k = 0; k < K; ++k)
+                ns += (bstart[l * (K + 1) + k + 1] - bstart[l * (K + 1) + k] + kSegLen - 1) / kSegLen;
+            seg0[l + 1] = seg0[l] + static_cast<int32_t>(ns);
+        }
+        long_seg0.assign(seg0.begin(), seg0.end());
+        seg_range.assign(seg0[nl], make_int2(0, 0));
+        // short-row tasks: spread over the block phases (their HBM misses
+        // overlap the L2-resident block phases) or all first
+        std::vector<int4> stasks;
+        std::vector<double> scost;
+        stasks.swap(tasks);
+        scost.swap(cost);
+        const size_t nst = stasks.size();
+        for (int k = 0; k < K; ++k) {
+            const size_t a0 = o.interleave ? nst * k / K : (k == 0 ? 0 : nst);
+            const size_t a1 = o.interleave ? nst * (k + 1) / K : nst;
+            for (size_t t = a0; t < a1; ++t) {
+                tasks.push_back(stasks[t]);
+                cost.push_back(scost[t]);
+            }
+            for (size_t l = 0; l < nl; ++l) {
+                const int64_t i = long_rows[l], e = bstart[l * (K + 1) + k + 1];
+                for (int64_t p = bstart[l * (K + 1) + k]; p < e; p += kSegLen) {
+                    const int kk = next[l]++;
+                    const int64_t pe = std::min<int64_t>(p + kSegLen, e);
+                    tasks.push_back(make_int4(static_cast<int>(i), static_cast<int>(l), TASK_L, kk));
+                    cost.push_back(static_cast<double>(pe - p) + 8.0);
+                    seg_range[seg0[l] + kk] = make_int2(static_cast<int>(p), static_cast<int>(pe));
+                }
+            }
+        }
+    } else {
+        long_seg0.push_back(nseg);
+    }
     // warp work units: consecutive tasks up to ~kGroupCost neighbour-equivalents
     // (at most kGroupTasks tasks); a hub segment is a unit of its own
     group_first.push_back(0);
@@ -157,9 +244,33 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
     g->nnz = nnz;
     std::vector<int32_t> rp32(rows + 1);
     for (int64_t i = 0; i <= rows; ++i) rp32[i] = static_cast<int32_t>(rp[i]);
+    // column blocking (spmm.cuh): binary operators whose C = 32 chunk of X
+    // exceeds ~4 slices; KZ_K1_SLICE_MB = 0 turns it off
+    SchedOpts so;
+    std::vector<int32_t> hcol;
+    {
+        const char* e = std::getenv("KZ_K1_SLICE_MB");
+        const double slice_mb = e ? std::atof(e) : kColBlockSliceMB;
+        const double chunk_mb = static_cast<double>(cols) * 32.0 * 8.0 / 1e6;
+        if (!vals && slice_mb > 0.0 && chunk_mb > 4.0 * slice_mb && nnz > 0) {
+            so.nblocks = static_cast<int>(std::ceil(chunk_mb / slice_mb));
+            if (const char* m = std::getenv("KZ_K1_MINDEG")) so.min_deg = std::atoll(m);
+            else so.min_deg = kColBlockMinDeg;
+            if (const char* m = std::getenv("KZ_K1_INTERLEAVE")) so.interleave = std::atoi(m);
+            hcol.resize(nnz);
+            cudaError_t ce = cudaMemcpy(hcol.data(), colidx, sizeof(int32_t) * nnz, cudaMemcpyDefault);
+            if (ce != cudaSuccess) return fail(KZ_ECUDA, std::string("colidx copy: ") + cudaGetErrorString(ce));
+            for (int64_t p = 0; p < nnz; ++p)
+                if (hcol[p] < 0 || hcol[p] >= cols) return fail(KZ_EARG, "column index out of range [0, cols)");
+        }
+    }
     std::vector<int4> tasks;
     std::vector<int32_t> long_seg0, group_first;
-    build_schedule(rp, rows, tasks, long_seg0, group_first, g->max_deg);
+    std::vector<int2> seg_range;
+    build_schedule(rp, rows, cols, hcol.empty() ? nullptr : hcol.data(), so, tasks, long_seg0, seg_range,
+                   group_first, g->max_deg);
+    g->nblocks = hcol.empty() ? 1 : so.nblocks;
+    if (!hcol.empty()) colidx = hcol.data();  // long rows regrouped by column block
     g->ngroups = static_cast<int32_t>(group_first.size()) - 1;
     g->ntasks = static_cast<int32_t>(tasks.size());
     g->nlong = static_cast<int32_t>(long_seg0.size()) - 1;
@@ -171,6 +282,7 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
         (st = upload(&g->tasks, tasks.data(), tasks.size())) ||
         (st = upload(&g->group_first, group_first.data(), group_first.size())) ||
         (st = upload(&g->long_seg0, long_seg0.data(), long_seg0.size())) ||
+        (st = upload(&g->seg_range, seg_range.data(), seg_range.size())) ||
         (vals && (st = upload(&g->vals, static_cast<const double*>(nullptr), nnz)))) {
         free_graph(g);
         return st;

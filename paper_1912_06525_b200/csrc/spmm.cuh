@@ -23,6 +23,11 @@
 //   L  one kSegLen-long segment of a long row (power-law hubs); the warp that
 //      runs a row's last segment waits for the others and combines the
 //      partial sums in segment order (stream-K style fix-up).
+// Optional column blocking (graph.cu SchedOpts, KZ_K1_SLICE_MB, off by
+// default): rows above a degree threshold are also cut by column block and
+// their segments run block-major so the gathered X slice stays in L2.
+// Measured at R-MAT 22 (profiles/r01_k1_colblock_sweep.jsonl): slower at
+// every slice size -- the per-segment fix-up costs more than the L2 hits save.
 // Each CTA owns a contiguous task range and its warps pull tasks dynamically
 // (no intra-CTA tail); every task's dot partial lands in its own shared slot
 // and slots are summed in task order, then CTAs in CTA order by the last CTA
@@ -43,6 +48,8 @@ constexpr int kGroupTasks = 8;   // max tasks a warp dequeues at once (one dot s
 constexpr double kGroupCost = 1024.0;  // max neighbour-equivalents per work unit
 constexpr int kSuperGroups = 256; // max groups reduced together by their last finisher
 constexpr int kSpmmMinBlocks = 5;
+constexpr double kColBlockSliceMB = 0.0;  // column-block slice of a C = 32 chunk (0: off)
+constexpr int64_t kColBlockMinDeg = 128;  // rows above this degree are column-blocked
 }  // namespace kz
 
 struct kz_graph {
@@ -57,6 +64,8 @@ struct kz_graph {
     int32_t nlong = 0;              // rows with deg > kSegLen
     int32_t nseg = 0;               // their segments
     int32_t* long_seg0 = nullptr;   // [nlong+1] first segment slot of each long row
+    int2* seg_range = nullptr;      // [nseg] CSR position range [x, y) of each segment
+    int32_t nblocks = 1;            // column blocks of the long-row phases (1: unblocked)
     int32_t max_deg = 0;
 };
 
@@ -207,6 +216,7 @@ struct SpmmArgs {
     const int4* __restrict__ tasks;
     const int32_t* __restrict__ group_first;
     const int32_t* __restrict__ long_seg0;
+    const int2* __restrict__ seg_range;
     int32_t ntasks, nlong, nseg;
     int32_t ngroups;    // task groups (kGroupTasks consecutive tasks) per chunk
     int32_t nsuper;     // super groups per chunk
@@ -388,8 +398,8 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
                 // long-row segment k of long row lidx
                 const int row = task.x, lidx = task.y, k = task.w;
                 const int s0 = a.long_seg0[lidx], nseg = a.long_seg0[lidx + 1] - s0;
-                const int beg = a.rowptr[row] + k * kSegLen;
-                const int end = min(beg + kSegLen, a.rowptr[row + 1]);
+                const int2 sr = a.seg_range[s0 + k];
+                const int beg = sr.x, end = sr.y;
                 double acc[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
@@ -554,6 +564,7 @@ inline SpmmArgs make_spmm_args(const kz_graph* g, const SpmmScratch& s) {
     a.colidx = g->colidx;
     a.tasks = g->tasks;
     a.long_seg0 = g->long_seg0;
+    a.seg_range = g->seg_range;
     a.ntasks = g->ntasks;
     a.nlong = g->nlong;
     a.nseg = g->nseg;
