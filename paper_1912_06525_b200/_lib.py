@@ -15,7 +15,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkatzb200.so")
+# KZ_LIB_PATH: an alternative build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("KZ_LIB_PATH") or os.path.join(_HERE, "libkatzb200.so")
 
 KZ_OK = 0
 KZ_EARG = 1

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kThreads)
     coldot_kernel(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows,
                   int64_t ldx, int64_t ldy, RedScratch red, int mode, SolveState s, double* out,
                   int iter) {
-    constexpr int VEC = Cfg<C>::VEC;
+    constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
     const double* Xb = X + static_cast<size_t>(chunk) * ldx;
     const double* Yb = Y + static_cast<size_t>(chunk) * ldy;
@@ -221,7 +221,7 @@ template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_update_kernel(double* __restrict__ r, const double* __restrict__ q, int64_t rows,
                      int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter) {
-    constexpr int VEC = Cfg<C>::VEC;
+    constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
     iter = cur_iter(s, iter);
     if (s.chunk_xstamp[chunk] != iter) return;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads)
     cg_pupdate_kernel(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ d,
                       int64_t rows, int64_t ldx, int64_t ldp, int64_t ldd, int nb, SolveState s,
                       int iter) {
-    constexpr int VEC = Cfg<C>::VEC;
+    constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / nb, local = blockIdx.x - chunk * nb;
     iter = cur_iter(s, iter);
     if (s.chunk_xstamp[chunk] != iter) return;

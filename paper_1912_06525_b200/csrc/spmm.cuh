@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -73,20 +74,39 @@ namespace kz {
 
 enum TaskType : int { TASK_S = 0, TASK_M = 1, TASK_L = 2 };
 
+#ifndef KZ_K1_VEC32
+#define KZ_K1_VEC32 2  // doubles per lane of a gathered row for C >= 32 (2: 16-byte, 4: 32-byte loads)
+#endif
+#ifndef KZ_K1_PRED
+#define KZ_K1_PRED 0   // 1: tail slots of a gather round are predicated off instead of clamped
+#endif
+#ifndef KZ_K1_R32
+#define KZ_K1_R32 0    // neighbours per round for C >= 32 (0: default rule)
+#endif
+
 template <int C>
 struct Cfg {
-    static constexpr int VEC = (C >= 2) ? 2 : 1;  // doubles per lane (16-byte loads)
+    // doubles per lane of a gathered row: 16-byte loads, or 32-byte
+    // (LDG.256, sm_100) loads for wide chunks
+    static constexpr int VEC = (C >= 32) ? KZ_K1_VEC32 : (C >= 2 ? 2 : 1);
+    static constexpr int SVEC = (C >= 2) ? 2 : 1;  // doubles per lane of the streaming kernels
     static constexpr int G = C / VEC;             // lanes per row group
     static constexpr int NGW = 32 / G;            // row groups per warp
     // neighbours gathered per round: 8 (4 for narrow groups) -- R*VEC doubles
     // of gather registers per lane
-    static constexpr int R = (G >= 8) ? 8 : (G >= 4 ? G : 4);
+    static constexpr int R = (C >= 32 && KZ_K1_R32 > 0) ? KZ_K1_R32 : ((G >= 8) ? (VEC == 4 ? 4 : 8) : (G >= 4 ? G : 4));
     static constexpr int PER = (R >= G) ? R / G : 1;  // indices loaded per lane per round
     static constexpr bool PART = R < G;               // only lanes lg < R load indices
 };
 
 template <int VEC>
 __device__ __forceinline__ void ld_nc(const double* p, double (&v)[VEC]);
+template <>
+__device__ __forceinline__ void ld_nc<4>(const double* p, double (&v)[4]) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+}
 template <>
 __device__ __forceinline__ void ld_nc<2>(const double* p, double (&v)[2]) {
     double2 t = __ldg(reinterpret_cast<const double2*>(p));
@@ -97,9 +117,39 @@ template <>
 __device__ __forceinline__ void ld_nc<1>(const double* p, double (&v)[1]) {
     v[0] = __ldg(p);
 }
+// Predicated gather: lanes with !pred issue no memory request and read 0.
+template <int VEC>
+__device__ __forceinline__ void ld_nc_pred(const double* p, double (&v)[VEC], bool pred) {
+    const int pr = pred;
+    if constexpr (VEC == 4) {
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+            "mov.f64 %0, 0d0000000000000000;\n\tmov.f64 %1, 0d0000000000000000;\n\t"
+            "mov.f64 %2, 0d0000000000000000;\n\tmov.f64 %3, 0d0000000000000000;\n\t"
+            "@q ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n\t}"
+            : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+            : "l"(p), "r"(pr));
+    } else if constexpr (VEC == 2) {
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+            "mov.f64 %0, 0d0000000000000000;\n\tmov.f64 %1, 0d0000000000000000;\n\t"
+            "@q ld.global.nc.v2.f64 {%0,%1}, [%2];\n\t}"
+            : "=d"(v[0]), "=d"(v[1])
+            : "l"(p), "r"(pr));
+    } else {
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+            "mov.f64 %0, 0d0000000000000000;\n\t"
+            "@q ld.global.nc.f64 %0, [%1];\n\t}"
+            : "=d"(v[0])
+            : "l"(p), "r"(pr));
+    }
+}
 template <int VEC>
 __device__ __forceinline__ void ld_plain(const double* p, double (&v)[VEC]) {
-    if constexpr (VEC == 2) {
+    if constexpr (VEC == 4) {
+        asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(p)
+                     : "memory");
+    } else if constexpr (VEC == 2) {
         double2 t = *reinterpret_cast<const double2*>(p);
         v[0] = t.x;
         v[1] = t.y;
@@ -109,7 +159,10 @@ __device__ __forceinline__ void ld_plain(const double* p, double (&v)[VEC]) {
 }
 template <int VEC>
 __device__ __forceinline__ void st_plain(double* p, const double (&v)[VEC]) {
-    if constexpr (VEC == 2) {
+    if constexpr (VEC == 4) {
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                     : "memory");
+    } else if constexpr (VEC == 2) {
         *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
     } else {
         *p = v[0];
@@ -120,7 +173,10 @@ __device__ __forceinline__ void st_plain(double* p, const double (&v)[VEC]) {
 // rows out of L2 (column indices are read with __ldcs for the same reason)
 template <int VEC>
 __device__ __forceinline__ void st_stream(double* p, const double (&v)[VEC]) {
-    if constexpr (VEC == 2) {
+    if constexpr (VEC == 4) {
+        asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                     : "memory");
+    } else if constexpr (VEC == 2) {
         __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
     } else {
         __stcs(p, v[0]);
@@ -174,7 +230,11 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
                 j = __shfl_sync(gmask, idx[t / K::G], gbase + (t % K::G));
                 if constexpr (W) w[t] = __shfl_sync(gmask, wv[t / K::G], gbase + (t % K::G));
             }
+#if KZ_K1_PRED
+            ld_nc_pred<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t], t < end - base);
+#else
             ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
+#endif
         }
         const int nvalid = end - base;  // slots t < nvalid hold real neighbours
 #pragma unroll
@@ -586,7 +646,12 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
     const int64_t total = static_cast<int64_t>(a.ngroups) * nchunks;
     if (total == 0) return KZ_OK;
     // persistent grid: at most one resident wave, at most one warp per group
-    const int64_t cap = static_cast<int64_t>(kNumSMs) * kSpmmMinBlocks;
+    static const int ctas_per_sm = [] {
+        const char* e = std::getenv("KZ_K1_CTAS");  // experiments: fewer resident CTAs per SM
+        const int v = e ? std::atoi(e) : kSpmmMinBlocks;
+        return v >= 1 && v <= kSpmmMinBlocks ? v : kSpmmMinBlocks;
+    }();
+    const int64_t cap = static_cast<int64_t>(kNumSMs) * ctas_per_sm;
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cap, (total + kWarps - 1) / kWarps)));
     a.nchunks = nchunks;
     a.nwarps = static_cast<int32_t>(grid) * kWarps;
