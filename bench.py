@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solver", default="eigen", choices=["eigen", "cg"])
+    ap.add_argument("--walk-terms", type=int, default=1, choices=[0, 1],
+                    help="eigen start: 1 = first Katz term exact + Galerkin on the remainder")
     return ap.parse_args()
 
 
@@ -188,7 +190,7 @@ def main():
     eidx, t_index = None, 0.0
     if args.solver == "eigen":
         t1 = time.perf_counter()
-        eidx = kz.EigenIndex(idx, spec["ell"])
+        eidx = kz.EigenIndex(idx, spec["ell"], walk_terms=args.walk_terms)
         t_index = time.perf_counter() - t1
     qidx = eidx if eidx is not None else idx
 
@@ -325,7 +327,9 @@ def main():
             "config": {"workload": workload, "n": n, "nnz": nnz, "beta": beta, "lambda_max": lam,
                        "queries_per_gpu": b, "top_k": k, "tol": tol,
                        "solver": (f"LRC-Katz, eigen form: rank-{eidx.rank} eigen index of A (low-rank Galerkin "
-                                  f"term, two fp64 DMMA GEMMs) + CG correction" if eidx is not None
+                                  f"term, two fp64 DMMA GEMMs"
+                                  + (", first Katz term beta*A*e_q exact via 2-walk counts" if eidx.walk_terms else "")
+                                  + ") + CG correction" if eidx is not None
                                   else "plain CG (query_cg_baseline)"),
                        "eigen_index_build_s": round(t_index, 2) if eidx is not None else None,
                        "mean_cg_iterations": mean_iters, "max_cg_iterations": int(np.max(iters_all)),

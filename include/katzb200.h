@@ -224,7 +224,11 @@ int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const in
  * but starts each column at the Galerkin point x0 = U W U' b with the exact
  * residual r0 = b - x0 + beta (AU)(W U' b) -- two tall-skinny fp64 DMMA
  * products, no SpMM -- then runs the reference's CG recurrence from there
- * with the stop test ||r|| <= tol ||b|| (solver.py:62-101). */
+ * with the stop test ||r|| <= tol ||b|| (solver.py:62-101).
+ * With a2u = A^2 U (optional) the start also carries the first Katz-series
+ * term exactly: x0 = beta A e_q + U y, y = beta^2 W (A^2 U)[q,:]', whose
+ * residual r0 = beta^2 A^2 e_q - U y + beta (AU) y needs only the 2-walk
+ * counts from q (an integer sparse push, no SpMM): one CG iteration fewer. */
 typedef struct kz_eigen kz_eigen;
 typedef struct kz_eigen_desc {
     int64_t n, r;
@@ -234,6 +238,7 @@ typedef struct kz_eigen_desc {
     const double* u;      /* device n x ldr row-major */
     const double* au;     /* device n x ldr row-major, A U */
     const double* w;      /* device r x r row-major, (I - beta U'AU)^-1 */
+    const double* a2u;    /* device n x ldr row-major, A^2 U; NULL: plain Galerkin start */
 } kz_eigen_desc;
 int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out);
 int kz_eigen_destroy(kz_eigen* h);

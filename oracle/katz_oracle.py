@@ -118,13 +118,19 @@ def query_cg_csr(a, beta, q, tol=1e-8, max_iter=None, start_seed=None):
 # ---------------------------------------------------------------------------
 
 
-def query_eigen_csr(a, beta, q, u, au, w, tol=1e-8, max_iter=None):
-    """Scores (clamped) and report of one query, eigen-form start + cg."""
+def query_eigen_csr(a, beta, q, u, au, w, tol=1e-8, max_iter=None, a2u=None):
+    """Scores (clamped) and report of one query, eigen-form start + cg.
+    With a2u (= A^2 U) the walk start: x0 = beta A e_q + U y with
+    y = beta^2 W (A^2 U)[q]' (the Galerkin step on the remainder)."""
     n = a.shape[0]
     rhs = np.zeros(n)
     rhs[a.indices[a.indptr[q] : a.indptr[q + 1]]] = beta
-    y = beta * (w @ au[q])
-    x0 = u @ y
+    if a2u is None:
+        y = beta * (w @ au[q])
+        x0 = u @ y
+    else:
+        y = (beta * beta) * (w @ a2u[q])
+        x0 = rhs + u @ y
     x, rep = cg(lambda v: v - beta * (a @ v), rhs, tol, max_iter, x0=x0)
     return np.maximum(x, 0.0), rep
 

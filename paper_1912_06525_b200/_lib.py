@@ -131,6 +131,7 @@ class KzEigenDesc(ctypes.Structure):
         ("u", ctypes.c_void_p),
         ("au", ctypes.c_void_p),
         ("w", ctypes.c_void_p),
+        ("a2u", ctypes.c_void_p),
     ]
 
 

@@ -176,6 +176,18 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_LAUNCH_CHECK();
         const int nt = w.bpad >= 64 ? 8 : w.bpad >= 32 ? 4 : w.bpad >= 16 ? 2 : 1;
         const size_t smem = lowrank_smem(eig->ldr, 8 * nt);
+        // walk start: 2-walk counts into the (still unused) q block, int32
+        int32_t* cnt = nullptr;
+        if (eig->a2u) {
+            cnt = reinterpret_cast<int32_t*>(w.q);
+            KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
+            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, (g->max_deg + 7) / 8))),
+                             static_cast<unsigned>(w.bpad));
+            KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
+                                                                                w.qpos, b);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+        }
         const int64_t ntiles = (n + kLrRows - 1) / kLrRows;
         const unsigned lgrid = static_cast<unsigned>(std::min<int64_t>(2 * kNumSMs, ntiles));
         for (int j0 = 0; j0 < w.bpad; j0 += 8 * nt) {
@@ -185,7 +197,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
             KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                          static_cast<int>(smem)));                                             \
             lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, w.p, n * CC, \
-                                                                            j0, w.bpad);                       \
+                                                                            j0, w.bpad, cnt);                  \
             ::kz::note_launch();                                                                               \
         });                                                                                                    \
     } while (0)
@@ -196,7 +208,9 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
 #undef KZ_LR
             KZ_LAUNCH_CHECK();
         }
-        KZ_DISPATCH_C(C, eigen_add_rhs_kernel<CC><<<w.bpad, kThreads, 0, st>>>(w.r, w.p, n * CC, g->rowptr, g->colidx,
+        // b = beta A e_q onto r0 and p0, or (walk start) onto x0
+        KZ_DISPATCH_C(C, eigen_add_rhs_kernel<CC><<<w.bpad, kThreads, 0, st>>>(cnt ? w.x : w.r, cnt ? nullptr : w.p,
+                                                                                n * CC, g->rowptr, g->colidx,
                                                                                 w.qpos, b, a->beta, s.bnorm2);
                       ::kz::note_launch());
         KZ_LAUNCH_CHECK();
@@ -307,6 +321,7 @@ extern "C" int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out) {
     h->u = d->u;
     h->au = d->au;
     h->w = d->w;
+    h->a2u = d->a2u;
     *out = h;
     return KZ_OK;
 }

@@ -11,6 +11,18 @@
 // CG then runs from (x0, r0) with the stop test ||r|| <= tol ||b|| -- the same
 // iterates as CG on M d = r0 from zero.  The two tall-skinny products
 // U y and (AU) y (n x r times r x b) are one fused DMMA pass.
+//
+// Walk start (a2u = A^2 U given): the first term of the Katz series
+// x = sum_k beta^k A^k e_q is put into the start exactly and the Galerkin
+// step is taken on the remainder,
+//     x0 = beta A e_q + U y,   y = beta^2 W (A^2 U)[q, :]'
+//     r0 = beta^2 A^2 e_q - U y + beta (AU) y,
+// where (A^2 e_q)_i = |N(i) ∩ N(q)| is an integer count (the 2-walks from q),
+// pushed from the neighbours of q with integer atomics -- order-free, so
+// deterministic -- at a cost of sum_{t in N(q)} deg(t) increments per query
+// (R-MAT 22: 45 M for 256 queries, vs 33 G gathered values for one SpMM).
+// The remainder's residual starts where plain Galerkin's first CG step
+// would leave it: one CG iteration fewer (R-MAT 22: 5 -> 4).
 #pragma once
 
 #include "spmm.cuh"
@@ -22,12 +34,14 @@ struct kz_eigen {
     const double* u = nullptr;      // device n x ldr row-major
     const double* au = nullptr;     // device n x ldr row-major
     const double* w = nullptr;      // device r x r row-major, symmetric
+    const double* a2u = nullptr;    // optional device n x ldr row-major, A^2 U (walk start)
 };
 
 namespace kz {
 
-// y[j] (chunked [nch][ldr][C]) = beta * W (AU)[q_j, :]'; padded columns and
-// rows r..ldr-1 are zero.  One thread per (k, j); fixed summation order.
+// y[j] (chunked [nch][ldr][C]) = beta * W (AU)[q_j, :]' (walk start:
+// beta^2 * W (A^2 U)[q_j, :]'); padded columns and rows r..ldr-1 are zero.
+// One thread per (k, j); fixed summation order.
 template <int C>
 __global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos, int b, double* __restrict__ y) {
     const int j = blockIdx.y;
@@ -35,10 +49,10 @@ __global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos
     if (k >= h.ldr) return;
     double s = 0.0;
     if (j < b && k < h.r) {
-        const double* __restrict__ aurow = h.au + qpos[j] * h.ldr;
+        const double* __restrict__ aurow = (h.a2u ? h.a2u : h.au) + qpos[j] * h.ldr;
         const double* __restrict__ wrow = h.w + k * h.r;
         for (int64_t i = 0; i < h.r; ++i) s = fma(wrow[i], __ldg(aurow + i), s);
-        s *= h.beta;
+        s *= h.a2u ? __dmul_rn(h.beta, h.beta) : h.beta;
     }
     y[static_cast<size_t>(j / C) * h.ldr * C + static_cast<size_t>(k) * C + (j % C)] = s;
 }
@@ -58,13 +72,16 @@ __device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double
 // are padding and are neither read nor written):
 //   x = U y ;  r = p = beta * (AU y) - x    (the rhs b = beta A e_q is added
 //   afterwards by eigen_add_rhs_kernel, so r is written, never read)
+// walk start (cnt != nullptr): r = p = beta * (AU y) - x + beta^2 * cnt with
+// cnt the int32 2-walk counts in the block layout; b goes onto x instead.
 // y's group columns are staged in shared memory once per CTA ([ldr][NC+8],
 // bank padded); each warp owns 16 rows of a 128-row tile and streams its U
 // and AU fragments from HBM kLrAhead k-steps ahead.  Persistent over tiles.
 template <int C, int NT>
 __global__ void __launch_bounds__(32 * kLrWarps, 2)
     lowrank_init_kernel(kz_eigen h, const double* __restrict__ y, double* __restrict__ x, double* __restrict__ r,
-                        double* __restrict__ p, int64_t ldv, int j0, int jmax) {
+                        double* __restrict__ p, int64_t ldv, int j0, int jmax,
+                        const int32_t* __restrict__ cnt = nullptr) {
     constexpr int NC = 8 * NT;
     constexpr int YLD = NC + 8;
     extern __shared__ __align__(16) double ys[];
@@ -144,7 +161,11 @@ __global__ void __launch_bounds__(32 * kLrWarps, 2)
                     const size_t off = static_cast<size_t>(j / C) * ldv + static_cast<size_t>(row) * C + (j % C);
                     const double x0 = ua[m][n][e];
                     x[off] = x0;
-                    const double r0 = __dsub_rn(__dmul_rn(h.beta, wa[m][n][e]), x0);
+                    double r0 = __dsub_rn(__dmul_rn(h.beta, wa[m][n][e]), x0);
+                    if (cnt) {
+                        const int32_t c = __ldcs(cnt + off);
+                        if (c) r0 = __dadd_rn(r0, __dmul_rn(__dmul_rn(h.beta, h.beta), static_cast<double>(c)));
+                    }
                     r[off] = r0;
                     p[off] = r0;
                 }
@@ -153,8 +174,9 @@ __global__ void __launch_bounds__(32 * kLrWarps, 2)
 }
 
 // r, p (chunked) += beta at the neighbours of q_j: the rhs b = beta A e_q
-// (index.py:93-101) added onto r0 = beta (AU) y - x0; and ||b||^2 =
-// beta^2 deg(q_j) for the stop threshold (solver.py:71-72).
+// (index.py:93-101) added onto r0 = beta (AU) y - x0 (walk start: x += beta
+// there instead, p == nullptr); and ||b||^2 = beta^2 deg(q_j) for the stop
+// threshold (solver.py:71-72).
 template <int C>
 __global__ void eigen_add_rhs_kernel(double* __restrict__ r, double* __restrict__ p, int64_t ld,
                                      const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
@@ -169,9 +191,30 @@ __global__ void eigen_add_rhs_kernel(double* __restrict__ r, double* __restrict_
     for (int k = beg + threadIdx.x; k < end; k += blockDim.x) {
         const size_t off = static_cast<size_t>(j / C) * ld + static_cast<size_t>(colidx[k]) * C + (j % C);
         r[off] = __dadd_rn(r[off], beta);
-        p[off] = __dadd_rn(p[off], beta);
+        if (p) p[off] = __dadd_rn(p[off], beta);
     }
     if (threadIdx.x == 0) bnorm2[j] = __dmul_rn(__dmul_rn(beta, beta), static_cast<double>(end - beg));
+}
+
+// 2-walk counts of the walk start: cnt[i, j] += 1 for every path q_j - t - i
+// (t in N(q_j)), i.e. cnt = A^2 e_q per column, in the chunked block layout
+// (int32, zeroed by the caller).  blockIdx.y = column; each warp takes one
+// neighbour t of q_j and pushes along N(t) with order-free integer atomics.
+template <int C>
+__global__ void walk2_count_kernel(int32_t* __restrict__ cnt, int64_t ld, const int32_t* __restrict__ rowptr,
+                                   const int32_t* __restrict__ colidx, const int64_t* __restrict__ qpos, int b) {
+    const int j = blockIdx.y;
+    if (j >= b) return;
+    const int64_t q = qpos[j];
+    const int beg = rowptr[q], end = rowptr[q + 1];
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    int32_t* __restrict__ base = cnt + static_cast<size_t>(j / C) * ld + (j % C);
+    for (int k = beg + static_cast<int>(blockIdx.x) * wpb + (threadIdx.x >> 5); k < end; k += gridDim.x * wpb) {
+        const int t = __ldg(colidx + k);
+        const int tb = __ldg(rowptr + t), te = __ldg(rowptr + t + 1);
+        for (int m = tb + lane; m < te; m += 32) atomicAdd(base + static_cast<size_t>(__ldg(colidx + m)) * C, 1);
+    }
 }
 
 inline size_t lowrank_smem(int64_t ldr, int NC) { return sizeof(double) * static_cast<size_t>(ldr) * (NC + 8); }

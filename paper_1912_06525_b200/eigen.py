@@ -19,6 +19,8 @@ solve order, same ids) and adds, in that order:
 * AU = A U: one K1 SpMM of the r-column block;
 * T = U'AU and W = (I - beta T)^-1 (r x r).
 
+* A2U = A (AU) (walk start, ``walk_terms=1``, the default): one more K1 SpMM.
+
 A query's low-rank term is the Galerkin point of span(U),
 x0 = U W U' b with U' b = beta (AU)[q, :]' -- exact for any orthonormal U, so
 Ritz-vector accuracy only changes iteration counts -- and the CG correction
@@ -26,6 +28,14 @@ runs from x0 with the exact residual r0 = b - x0 + beta (AU) W U' b; both
 products are the two tall-skinny fp64 DMMA GEMMs of ``lowrank_init_kernel``
 (one fused pass), then the reference's CG recurrence (solver.py:62-101) with
 the stop test ||r|| <= tol ||b||.
+
+Walk start (``walk_terms=1``): the first Katz-series term beta A e_q goes
+into the start exactly and the Galerkin step is taken on the remainder,
+x0 = beta A e_q + U y with y = beta^2 W (A^2 U)[q, :]', so
+r0 = beta^2 A^2 e_q - U y + beta (AU) y, where A^2 e_q is the integer count
+of 2-walks from q (a sparse push over the neighbours' lists, order-free
+integer atomics).  Measured effect: the CG correction needs one iteration
+fewer (R-MAT 16 prototype: 5 -> 4 at r = 128, 5.5 -> 4.5 at r = 32).
 """
 
 from __future__ import annotations
@@ -44,7 +54,7 @@ class EigenIndex:
 
     solver_kind = "eigen"
 
-    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM"):
+    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM", walk_terms=1):
         from .build import lanczos_topk
 
         if not isinstance(gi, GraphIndex):
@@ -59,6 +69,9 @@ class EigenIndex:
         rank = int(rank)
         if not 1 <= rank <= min(n, 384):
             raise ValueError(f"rank {rank} outside [1, min(n, 384)]")
+        if walk_terms not in (0, 1):
+            raise ValueError("walk_terms must be 0 (Galerkin start) or 1 (first Katz term exact)")
+        self.walk_terms = int(walk_terms)
         t0 = time.perf_counter()
         op = gi.operator()
 
@@ -77,25 +90,31 @@ class EigenIndex:
         ut[:r] = torch.as_tensor(np.ascontiguousarray(lr.vectors.T), device="cuda")
         aut = torch.zeros_like(ut)
         op.spmm(ut[:r].contiguous(), aut[:r], b=r, chunk=1)
+        a2ut = None
+        if self.walk_terms:
+            a2ut = torch.zeros_like(ut)
+            op.spmm(aut[:r].contiguous(), a2ut[:r], b=r, chunk=1)
         t = ut[:r] @ aut[:r].T
         t = 0.5 * (t + t.T)
         w = torch.linalg.inv(torch.eye(r, dtype=torch.float64, device="cuda") - self.alpha * t)
         self.u = ut.T.contiguous()      # n x ldr row-major
         self.au = aut.T.contiguous()    # n x ldr row-major
         self.w = w.contiguous()
+        self.a2u = a2ut.T.contiguous() if a2ut is not None else None  # n x ldr row-major
         self.ritz_values = lr.values.copy()
         self.rank, self.ldr = r, ldr
-        del ut, aut
+        del ut, aut, a2ut
         desc = _lib.KzEigenDesc()
         desc.n, desc.r, desc.ldr = n, r, ldr
         desc.beta = float(self.alpha)
         desc.op = op.handle.value
         desc.u, desc.au, desc.w = self.u.data_ptr(), self.au.data_ptr(), self.w.data_ptr()
+        desc.a2u = self.a2u.data_ptr() if self.a2u is not None else None
         h = ctypes.c_void_p()
         _lib.check(lib.kz_eigen_create(ctypes.byref(desc), ctypes.byref(h)))
         self._lib, self._handle = lib, h
         torch.cuda.synchronize()
-        self.build_stats = {"rank": r, "lanczos_seconds": t_lanczos,
+        self.build_stats = {"rank": r, "walk_terms": self.walk_terms, "lanczos_seconds": t_lanczos,
                             "build_seconds": time.perf_counter() - t0,
                             "ritz_top": [float(v) for v in lr.values[:4]]}
 
@@ -121,6 +140,15 @@ class EigenIndex:
         if inv is not None:
             u, au = u[inv], au[inv]
         return u, au, self.w.cpu().numpy()
+
+    def a2u_internal(self):
+        """A^2 U as a host array with rows in internal node order (None
+        without the walk start)."""
+        if self.a2u is None:
+            return None
+        a2u = self.a2u[:, : self.rank].cpu().numpy()
+        inv = getattr(self.gi, "_inv", None) if getattr(self.gi, "_order", None) is not None else None
+        return a2u[inv] if inv is not None else a2u
 
     # -- the GraphIndex surface (ids, operator, masks) ----------------------
     @property

@@ -40,14 +40,15 @@ def exact(a, alpha, internal):
     return np.asarray(spsolve(m, rhs)).reshape(a.shape[0], -1).T
 
 
+@pytest.mark.parametrize("walk", [0, 1])
 @pytest.mark.parametrize("beta", [0.5, 0.95])
 @pytest.mark.parametrize("rank,b", [(1, 1), (8, 5), (30, 37), (64, 64)])
 @pytest.mark.parametrize("tol", [1e-8, 1e-12])
-def test_eigen_start_matches_exact_solution(env, beta, rank, b, tol):
+def test_eigen_start_matches_exact_solution(env, beta, rank, b, tol, walk):
     kz, g, a, lmax, lmin = env
     alpha = beta / lmax
     gi = kz.GraphIndex(g, alpha=alpha, spectral_norm=lmax)
-    ei = kz.EigenIndex(gi, rank)
+    ei = kz.EigenIndex(gi, rank, walk_terms=walk)
     qs = g.original_ids[np.linspace(0, g.n - 1, b).astype(int)]
     scores, reps = kz.query_batch(ei, qs, tol=tol)
     _, reps_cg = kz.query_cg_baseline_batch(gi, qs, tol=tol)
@@ -125,8 +126,9 @@ def test_eigen_tiny_graphs_full_rank(env, edges, rank):
         assert reps[j].converged
 
 
+@pytest.mark.parametrize("walk", [0, 1])
 @pytest.mark.parametrize("reorder", [None, "rcm"])
-def test_eigen_matches_cpu_oracle_of_the_same_algorithm(env, reorder):
+def test_eigen_matches_cpu_oracle_of_the_same_algorithm(env, reorder, walk):
     """GPU eigen-form LRC against its CPU restatement (oracle.query_eigen_csr:
     the same basis, the reference's cg recurrence from the same start):
     rel L2 <= 1e-10 per column and iterations +/-1 -- the BASELINE parity bar
@@ -136,12 +138,40 @@ def test_eigen_matches_cpu_oracle_of_the_same_algorithm(env, reorder):
     kz, g, a, lmax, _ = env
     alpha = 0.5 / lmax
     gi = kz.GraphIndex(g, alpha=alpha, spectral_norm=lmax, reorder=reorder)
-    ei = kz.EigenIndex(gi, 16)
+    ei = kz.EigenIndex(gi, 16, walk_terms=walk)
     u, au, w = ei.basis_internal()
+    a2u = ei.a2u_internal()
+    assert (a2u is None) == (walk == 0)
     qs = g.original_ids[np.linspace(0, g.n - 1, 12).astype(int)]
     for tol in (1e-8, 1e-10):
         scores, reps = kz.query_batch(ei, qs, tol=tol)
         for j, q in enumerate(qs):
-            want, orep = O.query_eigen_csr(a.tocsr(), alpha, int(np.searchsorted(g.original_ids, q)), u, au, w, tol=tol)
+            want, orep = O.query_eigen_csr(a.tocsr(), alpha, int(np.searchsorted(g.original_ids, q)), u, au, w,
+                                           tol=tol, a2u=a2u)
             assert abs(reps[j].iterations - orep.iterations) <= 1, (j, reps[j].iterations, orep.iterations)
             assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
+
+
+def test_walk_start_saves_iterations_and_is_deterministic(env):
+    """The walk start (first Katz term exact + Galerkin on the remainder)
+    against the plain Galerkin start on the same basis: never more
+    iterations, fewer on average, same answer within cond * tol, and
+    bit-identical reruns (the 2-walk counts use order-free integer atomics)."""
+    import torch
+
+    kz, g, a, lmax, lmin = env
+    alpha = 0.5 / lmax
+    gi = kz.GraphIndex(g, alpha=alpha, spectral_norm=lmax)
+    e0 = kz.EigenIndex(gi, 32, walk_terms=0)
+    e1 = kz.EigenIndex(gi, 32, walk_terms=1)
+    qs = g.original_ids[np.linspace(0, g.n - 1, 64).astype(int)]
+    s0, r0 = kz.query_batch(e0, qs, tol=1e-8, device=True)
+    s1, r1 = kz.query_batch(e1, qs, tol=1e-8, device=True)
+    it0 = np.array([r.iterations for r in r0])
+    it1 = np.array([r.iterations for r in r1])
+    assert np.all(it1 <= it0) and it1.mean() < it0.mean(), (it0.mean(), it1.mean())
+    cond = (1 + alpha * abs(lmin)) / (1 - alpha * lmax)
+    diff = (torch.linalg.vector_norm(s1 - s0, dim=1) / torch.linalg.vector_norm(s0, dim=1)).cpu().numpy()
+    assert np.all(diff <= 2 * cond * 1e-8), diff.max()
+    s1b, _ = kz.query_batch(e1, qs, tol=1e-8, device=True)
+    assert torch.equal(s1, s1b)
