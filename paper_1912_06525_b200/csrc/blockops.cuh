@@ -216,17 +216,21 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // CG residual update (solver.py:88-90) fused with r.r:  r -= a*q for the
-// columns active in this iteration.
+// columns active in this iteration.  Sparse first iteration (cnt given, see
+// cg_sparse_pq_kernel): q = p - beta*A p is formed on the fly from p = r and
+// the 2-walk counts, (A p)_i = beta * cnt_i, with K1's epilogue roundings.
 template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_update_kernel(double* __restrict__ r, const double* __restrict__ q, int64_t rows,
-                     int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter) {
+                     int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter,
+                     const int32_t* __restrict__ cnt = nullptr, double beta = 0.0) {
     constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
     iter = cur_iter(s, iter);
     if (s.chunk_xstamp[chunk] != iter) return;
     r += static_cast<size_t>(chunk) * ldr;
     q += static_cast<size_t>(chunk) * ldq;
+    if (cnt) cnt += static_cast<size_t>(chunk) * ldq;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
     const size_t stride = static_cast<size_t>(red.nb) * kThreads;
     const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
@@ -245,7 +249,15 @@ __global__ void __launch_bounds__(kThreads)
     for (size_t pi = t0; pi < npairs; pi += stride) {
         double rv[VEC], qv[VEC];
         ld_plain<VEC>(r + pi * VEC, rv);
-        ld_plain<VEC>(q + pi * VEC, qv);
+        if (cnt) {
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                const int32_t c = __ldcs(cnt + pi * VEC + k);
+                qv[k] = __dadd_rn(rv[k], __dmul_rn(-beta, __dmul_rn(beta, static_cast<double>(c))));
+            }
+        } else {
+            ld_plain<VEC>(q + pi * VEC, qv);
+        }
 #pragma unroll
         for (int k = 0; k < VEC; ++k) {
             if (on[k]) rv[k] = __dsub_rn(rv[k], __dmul_rn(a[k], qv[k]));
@@ -258,6 +270,53 @@ __global__ void __launch_bounds__(kThreads)
     double total;
     if (chunk_last_reduce<C>(red, chunk, local, mine, sm, total))
         finalize_chunk<C>(mode, s, nullptr, chunk, iter, total);
+}
+
+// Sparse first CG iteration of a Katz solve from zero: p0 = r0 = b =
+// beta A e_q lives on N(q), so q0 = p0 - beta A p0 needs only
+// (A p0)_i = beta * cnt_i with cnt = A^2 e_q the 2-walk counts
+// (walk2_count_kernel), and p0.q0 is a sum over N(q).  One CTA per column:
+// the fixed-order p0.q0 and the K1 step-length hook (solver.py:83-87:
+// a = rs/pq, RuntimeError if pq <= 0); cg_update_kernel then forms q0 from
+// the counts.  Replaces the iteration's SpMM (R-MAT 22: 33 G gathered values)
+// by sum_{t in N(q)} deg(t) integer increments.
+template <int C>
+__global__ void __launch_bounds__(kThreads)
+    cg_sparse_pq_kernel(const double* __restrict__ r, const int32_t* __restrict__ cnt, int64_t ld,
+                        const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+                        const int64_t* __restrict__ qpos, double beta, SolveState s, int iter) {
+    const int j = blockIdx.x, chunk = j / C;
+    if (j % C == 0 && threadIdx.x == 0 && s.chunk_active[chunk]) s.chunk_xstamp[chunk] = iter;
+    if (j >= s.b || !s.active[j]) return;
+    const int64_t q = qpos[j];
+    const int beg = rowptr[q], end = rowptr[q + 1];
+    const size_t base = static_cast<size_t>(chunk) * ld + (j % C);
+    double acc = 0.0;
+    for (int k = beg + threadIdx.x; k < end; k += blockDim.x) {
+        const size_t off = base + static_cast<size_t>(colidx[k]) * C;
+        const double pv = r[off];
+        const double qv = __dadd_rn(pv, __dmul_rn(-beta, __dmul_rn(beta, static_cast<double>(cnt[off]))));
+        acc = fma(pv, qv, acc);
+    }
+    __shared__ double sm[kThreads];
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double v = sm[0];
+        if (v <= 0.0) {
+            s.status[j] = KZ_ENOTSPD;
+            s.active[j] = 0;
+            atomicExch(s.err, 1);
+            atomicSub(s.n_active, 1);
+        } else {
+            s.alpha[j] = s.rs[j] / v;
+            s.xstamp[j] = iter;
+        }
+    }
 }
 
 // Deferred solution update and new direction (solver.py:87, 95 / 144, 151):
@@ -288,6 +347,20 @@ __global__ void __launch_bounds__(kThreads)
         op[q] = ox[q] && s.active[col];
         a[q] = ox[q] ? s.alpha[col] : 0.0;
         bc[q] = op[q] ? s.betac[col] : 0.0;
+    }
+    // every column of the chunk stopped in this iteration's update (the last
+    // iteration): p is dead, so only x += a*p runs (3 block passes, not 5)
+    if (s.chunk_active && !s.chunk_active[chunk]) {
+        for (size_t pi = t0; pi < npairs; pi += stride) {
+            double xv[VEC], pv[VEC];
+            ld_plain<VEC>(x + pi * VEC, xv);
+            ld_plain<VEC>(p + pi * VEC, pv);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+                if (ox[k]) xv[k] = __dadd_rn(xv[k], __dmul_rn(a[k], pv[k]));
+            st_plain<VEC>(x + pi * VEC, xv);
+        }
+        return;
     }
     for (size_t pi = t0; pi < npairs; pi += stride) {
         double xv[VEC], pv[VEC], dv[VEC];

@@ -12,8 +12,15 @@
 // the reference order while saving one read+write of p and x per iteration.
 // The host only polls a device counter of active columns, one iteration
 // behind the GPU, so the device queue never drains.
+// A solve from zero with query-position rhs (b = beta A e_q) runs its first
+// iteration without the SpMM: p0 = b lives on N(q), so A p0 = beta A^2 e_q is
+// beta times the integer 2-walk counts (walk2_count_kernel), p0.q0 is a sum
+// over N(q) (cg_sparse_pq_kernel) and the update forms q0 from the counts.
+// The recurrence and its stop tests are unchanged; only the roundings of
+// q0's neighbour sums differ (beta*cnt instead of cnt repeated additions).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "driver.cuh"
@@ -221,7 +228,35 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
 
     const double work = static_cast<double>(g->nnz + n) * w.bpad;
     const int lag = work > 2e7 ? 1 : 3;
+    const bool use_graphs = work <= kGraphWork && graphs_enabled();
+    // a solve from zero with b = beta A e_q: the first iteration's SpMM is
+    // replaced by the 2-walk counts (cg_sparse_pq_kernel); KZ_CG_SPARSE_FIRST=0
+    // turns it off
+    const char* sf_env = std::getenv("KZ_CG_SPARSE_FIRST");
+    const bool sparse_first_on = !(sf_env && sf_env[0] == '0');
+    const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs;
     auto launch_iter = [&](int k) -> int {
+        if (k == 1 && sparse_first) {
+            int32_t* cnt = reinterpret_cast<int32_t*>(w.q);
+            KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
+            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, (g->max_deg + 7) / 8))),
+                             static_cast<unsigned>(w.bpad));
+            KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
+                                                                                w.qpos, b);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            KZ_DISPATCH_C(C, cg_sparse_pq_kernel<CC><<<w.bpad, kThreads, 0, st>>>(w.r, cnt, n * CC, g->rowptr,
+                                                                                  g->colidx, w.qpos, a->beta, s, k);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, n * CC, n * CC, w.red,
+                                                                              FIN_CG_CONV, s, k, cnt, a->beta);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, w.r, n, n * CC, n * CC, n * CC, nb, s, k); ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            return KZ_OK;
+        }
         SpmmArgs sa = make_spmm_args(g, w.sp);
         sa.Xg = w.p;
         sa.Xs = w.p;
@@ -254,8 +289,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     };
     int64_t ran = 0;
     // small solves are launch-bound: replay one captured iteration per step
-    int rc = work <= kGraphWork && graphs_enabled() ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
-                                                    : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
+    int rc = use_graphs ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
+                        : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
     if (rc) return rc;
 
     if (a->perm) {

@@ -205,6 +205,29 @@ def test_cg_batch_at_config_sizes(torch, kz, cfg):
         assert rel(scores[j].cpu().numpy(), want) <= REL_TOL
 
 
+@pytest.mark.parametrize("cfg", ["cfg1", "proxy16"])
+def test_cg_sparse_first_iteration_matches_dense(torch, kz, cfg, monkeypatch):
+    """The first CG iteration from zero runs on the 2-walk counts instead of
+    the SpMM (cg.cu, cg_sparse_pq_kernel): same iterates up to the roundings
+    of q0's neighbour sums -- identical iteration counts, scores within
+    1e-12 -- and run-to-run bit-identical."""
+    from paper_1912_06525_b200.generators import CONFIGS, config_graph, sample_queries
+
+    g = config_graph(cfg)
+    lam = kz.spectral_norm(g)
+    idx = kz.GraphIndex(g, 0.5 / lam)
+    qs = sample_queries(g.original_ids, CONFIGS[cfg]["b"], seed=1)
+    s1, r1 = kz.query_cg_baseline_batch(idx, qs, tol=1e-10, device=True)
+    s1b, _ = kz.query_cg_baseline_batch(idx, qs, tol=1e-10, device=True)
+    assert torch.equal(s1, s1b)
+    monkeypatch.setenv("KZ_CG_SPARSE_FIRST", "0")
+    s0, r0 = kz.query_cg_baseline_batch(idx, qs, tol=1e-10, device=True)
+    monkeypatch.delenv("KZ_CG_SPARSE_FIRST")
+    assert [r.iterations for r in r1] == [r.iterations for r in r0]
+    diff = (torch.linalg.vector_norm(s1 - s0, dim=1) / torch.linalg.vector_norm(s0, dim=1)).cpu().numpy()
+    assert np.all(diff <= 1e-12), diff.max()
+
+
 def test_topk_matches_lexsort(torch, kz):
     rng = np.random.default_rng(4)
     b, n = 7, 50_000
