@@ -188,7 +188,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         if (eig->a2u) {
             cnt = reinterpret_cast<int32_t*>(w.q);
             KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
-            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, (g->max_deg + 7) / 8))),
+            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, g->max_deg))),
                              static_cast<unsigned>(w.bpad));
             KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
                                                                                 w.qpos, b);
@@ -239,7 +239,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         if (k == 1 && sparse_first) {
             int32_t* cnt = reinterpret_cast<int32_t*>(w.q);
             KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
-            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, (g->max_deg + 7) / 8))),
+            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, g->max_deg))),
                              static_cast<unsigned>(w.bpad));
             KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
                                                                                 w.qpos, b);

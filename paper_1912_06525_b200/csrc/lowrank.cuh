@@ -198,22 +198,33 @@ __global__ void eigen_add_rhs_kernel(double* __restrict__ r, double* __restrict_
 
 // 2-walk counts of the walk start: cnt[i, j] += 1 for every path q_j - t - i
 // (t in N(q_j)), i.e. cnt = A^2 e_q per column, in the chunked block layout
-// (int32, zeroed by the caller).  blockIdx.y = column; each warp takes one
-// neighbour t of q_j and pushes along N(t) with order-free integer atomics.
+// (int32, zeroed by the caller).  blockIdx.y = column; each CTA takes one
+// neighbour t of q_j at a time and all its threads push along N(t) with
+// order-free integer atomics, 4 index loads in flight per thread (a hub
+// neighbour's list of ~10^5 entries is then ~100 rounds, not ~5,000).
 template <int C>
-__global__ void walk2_count_kernel(int32_t* __restrict__ cnt, int64_t ld, const int32_t* __restrict__ rowptr,
-                                   const int32_t* __restrict__ colidx, const int64_t* __restrict__ qpos, int b) {
+__global__ void __launch_bounds__(256) walk2_count_kernel(int32_t* __restrict__ cnt, int64_t ld,
+                                                          const int32_t* __restrict__ rowptr,
+                                                          const int32_t* __restrict__ colidx,
+                                                          const int64_t* __restrict__ qpos, int b) {
+    constexpr int U = 4;
     const int j = blockIdx.y;
     if (j >= b) return;
     const int64_t q = qpos[j];
     const int beg = rowptr[q], end = rowptr[q + 1];
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
     int32_t* __restrict__ base = cnt + static_cast<size_t>(j / C) * ld + (j % C);
-    for (int k = beg + static_cast<int>(blockIdx.x) * wpb + (threadIdx.x >> 5); k < end; k += gridDim.x * wpb) {
+    for (int k = beg + static_cast<int>(blockIdx.x); k < end; k += gridDim.x) {
         const int t = __ldg(colidx + k);
         const int tb = __ldg(rowptr + t), te = __ldg(rowptr + t + 1);
-        for (int m = tb + lane; m < te; m += 32) atomicAdd(base + static_cast<size_t>(__ldg(colidx + m)) * C, 1);
+        int m = tb + threadIdx.x;
+        for (; m + (U - 1) * static_cast<int>(blockDim.x) < te; m += U * blockDim.x) {
+            int i[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) i[u] = __ldcs(colidx + m + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < U; ++u) atomicAdd(base + static_cast<size_t>(i[u]) * C, 1);
+        }
+        for (; m < te; m += blockDim.x) atomicAdd(base + static_cast<size_t>(__ldcs(colidx + m)) * C, 1);
     }
 }
 
