@@ -307,7 +307,8 @@ def main():
         threads = len(os.sched_getaffinity(0))
         qps, done, dt, it = cpu_sample(g, beta, qs, tol, args.cpu_budget, threads)
         cpu = {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
-               "sample": f"{done} of the {b} bench queries ({workload}), oracle CSR cg "
+               "sample": f"{done} query solves ({min(done, b)} distinct of the {b} bench queries, cycled; "
+                         f"{workload}), oracle CSR cg "
                          f"(reference solver.py:62-101 recurrence) on {threads} host threads, {dt:.1f} s"}
 
     if rank == 0:
