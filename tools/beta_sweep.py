@@ -4,7 +4,8 @@ beta in {0.1, 0.5, 0.9, 0.99} x 1/lambda_max, correction rank r in {32, 128},
 a batch of 64 seeded queries, fp64, tol 1e-8: LRC-Katz (Schur PCG on an index
 built on the device by build.py -- the reference's CPU build cannot hold the
 ~24 GB separator factor) against plain CG (GraphIndex), iteration counts and
-queries/sec.  Each LRC batch is also checked against the CG batch (both
+queries/sec, plus the north-star eigen form (EigenIndex, walk start) at the
+same rank.  Each LRC / eigen batch is also checked against the CG batch (all
 converge to tol 1e-8, so they agree to ~cond * 1e-8).
 
     python tools/beta_sweep.py [--betas 0.1,0.5,0.9,0.99] [--ranks 32,128]
@@ -80,6 +81,20 @@ def main():
                 "cg_iters_max": int(max(r.iterations for r in r_cg)),
                 "lrc_vs_cg_max_rel_l2": float(diff),
             }
+            # the north-star eigen form (EigenIndex, walk start) at the same rank
+            ei = kz.EigenIndex(gi, ell)
+            dt_e, (s_e, r_e) = timed(lambda: kz.query_batch(ei, qs, tol=1e-8, device=True), args.reps)
+            s_e = s_e.cpu().numpy()
+            rec.update({
+                "eigen_build_seconds": round(ei.build_stats["build_seconds"], 2),
+                "eigen_qps": round(args.b / dt_e, 1), "eigen_ms": round(dt_e * 1e3, 2),
+                "eigen_iters_mean": float(np.mean([r.iterations for r in r_e])),
+                "eigen_iters_max": int(max(r.iterations for r in r_e)),
+                "eigen_converged": all(r.converged for r in r_e),
+                "eigen_vs_cg_max_rel_l2": float(max(np.linalg.norm(a - c) / np.linalg.norm(c)
+                                                    for a, c in zip(s_e, s_cg))),
+            })
+            del ei
             print(json.dumps(rec), flush=True)
             lines.append(rec)
             del idx
