@@ -75,7 +75,10 @@ namespace kz {
 enum TaskType : int { TASK_S = 0, TASK_M = 1, TASK_L = 2 };
 
 #ifndef KZ_K1_VEC32
-#define KZ_K1_VEC32 2  // doubles per lane of a gathered row for C >= 32 (2: 16-byte, 4: 32-byte loads)
+#define KZ_K1_VEC32 4  // doubles per lane of a gathered row for C >= 32 (2: 16-byte, 4: 32-byte loads)
+#endif
+#ifndef KZ_K1_SMEM_DOT
+#define KZ_K1_SMEM_DOT 1  // 1: column-dot accumulators in shared memory instead of registers
 #endif
 #ifndef KZ_K1_PRED
 #define KZ_K1_PRED 0   // 1: tail slots of a gather round are predicated off instead of clamped
@@ -394,9 +397,17 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         const int chunk = g / a.ngroups, gl = g - chunk * a.ngroups;
         if (a.chunk_active && !a.chunk_active[chunk]) continue;
         const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.ldxg;
+#if KZ_K1_SMEM_DOT
+        // the column-dot accumulators live in shared memory (one slot per
+        // thread), not in registers across the gather loop
+        __shared__ double s_dacc[VEC * kThreads];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) s_dacc[q * kThreads + threadIdx.x] = 0.0;
+#else
         double dacc[VEC];
 #pragma unroll
         for (int q = 0; q < VEC; ++q) dacc[q] = 0.0;
+#endif
 
         auto epilogue = [&](int row, const double (&acc)[VEC]) {
             const size_t roff = static_cast<size_t>(row) * C + lg * VEC;
@@ -423,7 +434,14 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
                 ld_plain<VEC>(a.D ? a.D + static_cast<size_t>(chunk) * a.ldd + roff
                                   : a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, d);
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) dacc[q] = fma(d[q], y[q], dacc[q]);
+                for (int q = 0; q < VEC; ++q) {
+#if KZ_K1_SMEM_DOT
+                    double& da = s_dacc[q * kThreads + threadIdx.x];
+                    da = fma(d[q], y[q], da);
+#else
+                    dacc[q] = fma(d[q], y[q], dacc[q]);
+#endif
+                }
             }
         };
         auto warp_sum = [&](double (&v)[VEC]) {
@@ -502,6 +520,11 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         if (!a.want_dot) continue;
 
         // ---- deterministic dot reduction: group -> super group -> chunk ----
+#if KZ_K1_SMEM_DOT
+        double dacc[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) dacc[q] = s_dacc[q * kThreads + threadIdx.x];
+#endif
         warp_sum(dacc);
         double* gs = a.gslot + (static_cast<size_t>(chunk) * a.ngroups + gl) * C;
         if (lane < K::G) {
