@@ -48,7 +48,10 @@ constexpr int kSegLen = 1024;    // rows with deg > kSegLen are split into segme
 constexpr int kGroupTasks = 8;   // max tasks a warp dequeues at once (one dot slot)
 constexpr double kGroupCost = 1024.0;  // max neighbour-equivalents per work unit
 constexpr int kSuperGroups = 256; // max groups reduced together by their last finisher
-constexpr int kSpmmMinBlocks = 5;
+#ifndef KZ_K1_MINBLOCKS
+#define KZ_K1_MINBLOCKS 5  // resident CTAs per SM the register budget is sized for
+#endif
+constexpr int kSpmmMinBlocks = KZ_K1_MINBLOCKS;
 constexpr double kColBlockSliceMB = 0.0;  // column-block slice of a C = 32 chunk (0: off)
 constexpr int64_t kColBlockMinDeg = 128;  // rows above this degree are column-blocked
 }  // namespace kz
