@@ -112,6 +112,104 @@ __global__ void __launch_bounds__(W * 32, 1) tma_gather(const double* __restrict
     if (acc == 12345.678) sink[0] = acc;
 }
 
+// Mixed: warps < NL gather with 16-byte LDGs (K1 scheme), the others with
+// per-row TMA bulk copies into a 1-stage smem ring; all pull 512-row batches
+// from one atomic queue, so the two paths run concurrently to the end.
+template <int NW, int NL>
+__global__ void __launch_bounds__(NW * 32, 1) mixed_gather(const double* __restrict__ rows, const int* __restrict__ idx,
+                                                          size_t nidx, int* queue, double* sink) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[NW];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr size_t kBatch = 512;
+    const size_t nbatch = (nidx + kBatch - 1) / kBatch;
+    double acc = 0.0;
+    if (warp < NL) {
+        const int lg = lane & 15, grp = lane >> 4;
+        const double2* r2 = reinterpret_cast<const double2*>(rows);
+        double2 a2 = make_double2(0.0, 0.0);
+        while (true) {
+            int bi = 0;
+            if (lane == 0) bi = atomicAdd(queue, 1);
+            bi = __shfl_sync(0xffffffffu, bi, 0);
+            if (static_cast<size_t>(bi) >= nbatch) break;
+            const size_t b0 = static_cast<size_t>(bi) * kBatch;
+            const size_t b1 = b0 + kBatch < nidx ? b0 + kBatch : nidx;
+            for (size_t base = b0; base < b1; base += 16) {
+                const size_t k = base + grp * 8 + (lg & 7);
+                const int j = k < b1 ? __ldg(idx + k) : 0;
+                double2 v[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int jt = __shfl_sync(0xffffffffu, j, grp * 16 + t);
+                    v[t] = __ldg(r2 + static_cast<size_t>(jt) * 16 + lg);
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    a2.x += v[t].x;
+                    a2.y += v[t].y;
+                }
+            }
+        }
+        acc = a2.x + a2.y;
+    } else {
+        double* ring = reinterpret_cast<double*>(smem) + static_cast<size_t>(warp - NL) * 32 * 32;
+        if (lane == 0) mbar_init(&bars[warp], 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        uint32_t phase = 0;
+        while (true) {
+            int bi = 0;
+            if (lane == 0) bi = atomicAdd(queue, 1);
+            bi = __shfl_sync(0xffffffffu, bi, 0);
+            if (static_cast<size_t>(bi) >= nbatch) break;
+            const size_t b0 = static_cast<size_t>(bi) * kBatch;
+            const size_t b1 = b0 + kBatch < nidx ? b0 + kBatch : nidx;
+            for (size_t base = b0; base < b1; base += 32) {
+                const int nv = static_cast<int>(b1 - base < 32 ? b1 - base : 32);
+                if (lane == 0) mbar_expect(&bars[warp], nv * 256u);
+                __syncwarp();
+                if (lane < nv)
+                    bulk_g2s(ring + static_cast<size_t>(lane) * 32, rows + static_cast<size_t>(__ldg(idx + base + lane)) * 32,
+                             256u, &bars[warp]);
+                mbar_wait(&bars[warp], phase);
+                phase ^= 1;
+                for (int t = 0; t < nv; ++t) acc += ring[t * 32 + lane];
+                __syncwarp();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+        }
+    }
+    if (acc == 12345.678) sink[0] = acc;
+}
+
+template <int NW, int NL>
+float run_mixed(const double* rows, const int* idx, size_t nidx, double* sink, int sms) {
+    const size_t smem = static_cast<size_t>(NW - NL) * 32 * 256 + 16;
+    cudaFuncSetAttribute(mixed_gather<NW, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int* q;
+    cudaMalloc(&q, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMemset(q, 0, 4);
+    mixed_gather<NW, NL><<<sms, NW * 32, smem>>>(rows, idx, nidx, q, sink);
+    cudaMemset(q, 0, 4);
+    cudaEventRecord(e0);
+    mixed_gather<NW, NL><<<sms, NW * 32, smem>>>(rows, idx, nidx, q, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        printf("error %s\n", cudaGetErrorString(e));
+        exit(1);
+    }
+    cudaFree(q);
+    return ms;
+}
+
 template <int W, int S>
 float run_tma(const double* rows, const int* idx, size_t nidx, double* sink, int sms) {
     const size_t smem = static_cast<size_t>(W) * S * 32 * 256;
@@ -174,7 +272,11 @@ int main() {
         printf(", \"tma_w4_s6\": %.2f", gb / run_tma<4, 6>(rows, idx, nidx, sink, sms));
         printf(", \"tma_w12_s2\": %.2f", gb / run_tma<12, 2>(rows, idx, nidx, sink, sms));
         printf(", \"tma_w16_s1\": %.2f", gb / run_tma<16, 1>(rows, idx, nidx, sink, sms));
-        printf(", \"tma_w6_s4\": %.2f}", gb / run_tma<6, 4>(rows, idx, nidx, sink, sms));
+        printf(", \"tma_w6_s4\": %.2f", gb / run_tma<6, 4>(rows, idx, nidx, sink, sms));
+        printf(", \"mixed_32w_ldg32\": %.2f", gb / run_mixed<32, 32>(rows, idx, nidx, sink, sms));
+        printf(", \"mixed_32w_ldg24_tma8\": %.2f", gb / run_mixed<32, 24>(rows, idx, nidx, sink, sms));
+        printf(", \"mixed_32w_ldg16_tma16\": %.2f", gb / run_mixed<32, 16>(rows, idx, nidx, sink, sms));
+        printf(", \"mixed_32w_ldg28_tma4\": %.2f}", gb / run_mixed<32, 28>(rows, idx, nidx, sink, sms));
         fflush(stdout);
         cudaFree(rows);
         cudaFree(idx);
