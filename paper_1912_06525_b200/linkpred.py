@@ -98,11 +98,12 @@ def katz_rank_batch(idx, qs, s, tol=1e-10):
     s_eff = min(int(s), idx.n)
     ids, vals, counts = topk_device(scores, s_eff, idx.mask_operator(), internal, internal)
     ids, vals, counts = ids.cpu().numpy(), vals.cpu().numpy(), counts.cpu().numpy()
+    orig = np.asarray(idx.id_map)[np.maximum(ids, 0)]  # internal -> original ids, one gather
     out = []
-    for j, q in enumerate(qs):
+    for j, q in enumerate(qs.tolist()):
         m = int(counts[j])
-        cands = [(int(idx.id_map[ids[j, c]]), float(vals[j, c])) for c in range(m)]
-        out.append(RankedPrediction(query=int(q), candidates=cands, method="katz"))
+        cands = list(zip(orig[j, :m].tolist(), vals[j, :m].tolist()))
+        out.append(RankedPrediction(query=q, candidates=cands, method="katz"))
     return out
 
 
@@ -170,11 +171,12 @@ def sparse_katz_batch(idx, qs, s, T=None, tol=1e-10, anchor_batch=256):
     top_h, corr_h, order_h, counts_h = (top.cpu().numpy(), corr.cpu().numpy(), order.cpu().numpy(),
                                         counts.cpu().numpy())
     out = []
-    for j, q in enumerate(qs):
+    for j, q in enumerate(qs.tolist()):
         m = int(counts_h[j])
-        cands = [(int(idx.id_map[top_h[j, order_h[j, c]]]), float(corr_h[j, order_h[j, c]]))
-                 for c in range(m)]
-        out.append(RankedPrediction(query=int(q), candidates=cands, method="sparse-katz"))
+        o = order_h[j, :m]
+        ids_j = np.asarray(idx.id_map)[top_h[j, o]]
+        cands = list(zip(ids_j.tolist(), corr_h[j, o].tolist()))
+        out.append(RankedPrediction(query=q, candidates=cands, method="sparse-katz"))
     return out
 
 
