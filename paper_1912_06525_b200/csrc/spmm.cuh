@@ -688,8 +688,19 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
     if (a.ldd == 0) a.ldd = g->rows * C;
     a.vals = g->vals;
     const bool w = g->vals != nullptr;
+    // experiments: KZ_K1_CARVEOUT = preferred shared-memory carveout (percent)
+    static const int carveout = [] {
+        const char* e = std::getenv("KZ_K1_CARVEOUT");
+        return e ? std::atoi(e) : -1;
+    }();
 #define KZ_SPMM_CASE(CC)                                                                  \
     case CC:                                                                              \
+        if (carveout >= 0) {                                                              \
+            cudaFuncSetAttribute(spmm_kernel<CC, true>,                                   \
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, carveout); \
+            cudaFuncSetAttribute(spmm_kernel<CC, false>,                                  \
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, carveout); \
+        }                                                                                 \
         if (w) spmm_kernel<CC, true><<<grid, kThreads, 0, st>>>(a);                        \
         else spmm_kernel<CC, false><<<grid, kThreads, 0, st>>>(a);                         \
         break;
