@@ -90,6 +90,37 @@ def test_spmm_matches_scipy(torch, kz, graph, b, C):
     assert torch.equal(Yd, Y2)
 
 
+@pytest.mark.parametrize("slice_mb,min_deg", [(0.002, 40), (0.01, 128), (0.002, 1024)])
+def test_spmm_column_blocked_schedule(torch, kz, monkeypatch, slice_mb, min_deg):
+    """The opt-in column-blocked long-row schedule of K1 (graph.cu SchedOpts,
+    forced here by a tiny KZ_K1_SLICE_MB): same operator, short rows still
+    bit-exact against scipy, the rest within roundoff, deterministic."""
+    from paper_1912_06525_b200.generators import rmat_graph
+
+    g = rmat_graph(12, seed=3)
+    n, off, col = g.n, g.row_offsets, g.col_indices
+    a = O.csr_matrix(off, col, n)
+    monkeypatch.setenv("KZ_K1_SLICE_MB", str(slice_mb))
+    monkeypatch.setenv("KZ_K1_MINDEG", str(min_deg))
+    op = kz.DeviceOperator(off, col.astype(np.int32), n)
+    monkeypatch.delenv("KZ_K1_SLICE_MB")
+    b, C = 32, 32
+    X = np.random.default_rng(5).standard_normal((n, b))
+    Xd = torch.as_tensor(to_blk(X, C)).cuda()
+    Yd = torch.empty_like(Xd)
+    dots = torch.empty(b, dtype=torch.float64, device="cuda")
+    op.spmm(Xd, Yd, b=b, chunk=C, Xs=Xd, s1=1.0, s2=-0.01, dots=dots)
+    Y = from_blk(Yd.cpu().numpy(), n, b, C)
+    want = X - 0.01 * (a @ X)
+    short = np.diff(off) <= 32
+    assert np.array_equal(Y[short], want[short])
+    assert np.abs(Y - want).max() <= 1e-13 * np.abs(want).max()
+    assert np.allclose(dots.cpu().numpy(), np.einsum("ij,ij->j", X, want), rtol=1e-12, atol=0)
+    Y2 = torch.empty_like(Xd)
+    op.spmm(Xd, Y2, b=b, chunk=C, Xs=Xd, s1=1.0, s2=-0.01)
+    assert torch.equal(Yd, Y2)
+
+
 def test_cg_batch_matches_reference_cg_golden(torch, kz):
     rec, n = chunglu_fixture()
     g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"],
