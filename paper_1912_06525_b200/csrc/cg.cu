@@ -234,7 +234,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     // turns it off
     const char* sf_env = std::getenv("KZ_CG_SPARSE_FIRST");
     const bool sparse_first_on = !(sf_env && sf_env[0] == '0');
-    const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs;
+    const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs &&
+                              w.bpad <= 65535;  // one grid row per column in walk2_count_kernel
     auto launch_iter = [&](int k) -> int {
         if (k == 1 && sparse_first) {
             int32_t* cnt = reinterpret_cast<int32_t*>(w.q);
