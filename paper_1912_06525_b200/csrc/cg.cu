@@ -196,7 +196,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
             KZ_LAUNCH_CHECK();
         }
         const int64_t ntiles = (n + kLrRows - 1) / kLrRows;
-        const unsigned lgrid = static_cast<unsigned>(std::min<int64_t>(2 * kNumSMs, ntiles));
+        const unsigned lgrid = static_cast<unsigned>(std::min<int64_t>(KZ_LR_MINBLOCKS * kNumSMs, ntiles));
         for (int j0 = 0; j0 < w.bpad; j0 += 8 * nt) {
 #define KZ_LR(NN)                                                                                              \
     do {                                                                                                       \

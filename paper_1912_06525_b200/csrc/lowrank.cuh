@@ -60,7 +60,13 @@ __global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos
 constexpr int kLrWarps = 8;
 constexpr int kLrMT = 1;                           // m-fragments (8 rows) per warp (2 spills)
 constexpr int kLrRows = 8 * kLrMT * kLrWarps;      // rows per tile
-constexpr int kLrAhead = 4;                        // k-steps of A fragments in flight
+#ifndef KZ_LR_AHEAD
+#define KZ_LR_AHEAD 4
+#endif
+#ifndef KZ_LR_MINBLOCKS
+#define KZ_LR_MINBLOCKS 2
+#endif
+constexpr int kLrAhead = KZ_LR_AHEAD;              // k-steps of A fragments in flight
 
 __device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -78,7 +84,7 @@ __device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double
 // bank padded); each warp owns 16 rows of a 128-row tile and streams its U
 // and AU fragments from HBM kLrAhead k-steps ahead.  Persistent over tiles.
 template <int C, int NT>
-__global__ void __launch_bounds__(32 * kLrWarps, 2)
+__global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
     lowrank_init_kernel(kz_eigen h, const double* __restrict__ y, double* __restrict__ x, double* __restrict__ r,
                         double* __restrict__ p, int64_t ldv, int j0, int jmax,
                         const int32_t* __restrict__ cnt = nullptr) {
