@@ -223,7 +223,8 @@ template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_update_kernel(double* __restrict__ r, const double* __restrict__ q, int64_t rows,
                      int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter,
-                     const int32_t* __restrict__ cnt = nullptr, double beta = 0.0) {
+                     const int32_t* __restrict__ cnt = nullptr, double beta = 0.0,
+                     double* __restrict__ r_out = nullptr) {
     constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
     iter = cur_iter(s, iter);
@@ -231,6 +232,8 @@ __global__ void __launch_bounds__(kThreads)
     r += static_cast<size_t>(chunk) * ldr;
     q += static_cast<size_t>(chunk) * ldq;
     if (cnt) cnt += static_cast<size_t>(chunk) * ldq;
+    // history mode: r_{k+1} goes to its own slot, r_k stays for the final x
+    double* __restrict__ ro = r_out ? r_out + static_cast<size_t>(chunk) * ldr : r;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
     const size_t stride = static_cast<size_t>(red.nb) * kThreads;
     const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(kThreads)
             if (on[k]) rv[k] = __dsub_rn(rv[k], __dmul_rn(a[k], qv[k]));
             acc[k] = fma(rv[k], rv[k], acc[k]);
         }
-        st_plain<VEC>(r + pi * VEC, rv);
+        st_plain<VEC>(ro + pi * VEC, rv);
     }
     __shared__ double sm[kThreads];
     const double mine = block_col_reduce<C, VEC>(acc, sm);
@@ -326,12 +329,23 @@ template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_pupdate_kernel(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ d,
                       int64_t rows, int64_t ldx, int64_t ldp, int64_t ldd, int nb, SolveState s,
-                      int iter) {
+                      int iter, double* __restrict__ ahist = nullptr, double* __restrict__ bhist = nullptr) {
     constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / nb, local = blockIdx.x - chunk * nb;
     iter = cur_iter(s, iter);
     if (s.chunk_xstamp[chunk] != iter) return;
-    x += static_cast<size_t>(chunk) * ldx;
+    // history mode (x == nullptr): record this iteration's step length and
+    // direction coefficient per column; x is formed at the end from the
+    // residual history (cg_hist_coef_kernel / cg_hist_sum)
+    if (ahist && local == 0 && threadIdx.x < C) {
+        const int col = chunk * C + threadIdx.x;
+        if (col < s.b) {
+            const bool on = s.xstamp[col] == iter;
+            ahist[col] = on ? s.alpha[col] : 0.0;
+            bhist[col] = on && s.active[col] ? s.betac[col] : 0.0;
+        }
+    }
+    if (x) x += static_cast<size_t>(chunk) * ldx;
     p += static_cast<size_t>(chunk) * ldp;
     d += static_cast<size_t>(chunk) * ldd;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
@@ -351,6 +365,7 @@ __global__ void __launch_bounds__(kThreads)
     // every column of the chunk stopped in this iteration's update (the last
     // iteration): p is dead, so only x += a*p runs (3 block passes, not 5)
     if (s.chunk_active && !s.chunk_active[chunk]) {
+        if (!x) return;  // history mode: nothing left to do for this chunk
         for (size_t pi = t0; pi < npairs; pi += stride) {
             double xv[VEC], pv[VEC];
             ld_plain<VEC>(x + pi * VEC, xv);
@@ -359,6 +374,19 @@ __global__ void __launch_bounds__(kThreads)
             for (int k = 0; k < VEC; ++k)
                 if (ox[k]) xv[k] = __dadd_rn(xv[k], __dmul_rn(a[k], pv[k]));
             st_plain<VEC>(x + pi * VEC, xv);
+        }
+        return;
+    }
+    if (!x) {
+        // history mode: p = d + betac*p only (3 block passes)
+        for (size_t pi = t0; pi < npairs; pi += stride) {
+            double pv[VEC], dv[VEC];
+            ld_plain<VEC>(p + pi * VEC, pv);
+            ld_plain<VEC>(d + pi * VEC, dv);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+                if (op[k]) pv[k] = __dadd_rn(dv[k], __dmul_rn(bc[k], pv[k]));
+            st_plain<VEC>(p + pi * VEC, pv);
         }
         return;
     }
@@ -374,6 +402,57 @@ __global__ void __launch_bounds__(kThreads)
         }
         st_plain<VEC>(x + pi * VEC, xv);
         st_plain<VEC>(p + pi * VEC, pv);
+    }
+}
+
+// ---- residual-history form of the solution update ---------------------------
+// With p_0 = r_0 and p_{k+1} = r_{k+1} + beta_k p_k, the CG iterate is
+//   x_K = x_0 + sum_{k<K} a_k p_k = x_0 + sum_{i<K} c_i r_i,
+//   c_{K-1} = a_{K-1},  c_i = a_i + beta_i c_{i+1},
+// so while the residuals r_0..r_{H-1} are kept in their own slots the loop
+// never touches x (saving its read + write every iteration), and x is formed
+// once -- in the output gather, or by a fold when a solve outgrows the slots.
+struct CgHistory {
+    const double* slots = nullptr;  // [H] blocks of the chunked layout, slot stride `slot`
+    size_t slot = 0;                // elements between slots
+    const double* coef = nullptr;   // [H][bpad] c_i per column
+    const int32_t* kcol = nullptr;  // [bpad] residuals used per column
+    const double* x0 = nullptr;     // start block, or nullptr (x_0 = 0)
+    int bpad = 0;
+};
+
+// element e (chunked offset) of column col
+__device__ __forceinline__ double hist_value(const CgHistory& h, size_t e, int col) {
+    double v = h.x0 ? h.x0[e] : 0.0;
+    const int kc = h.kcol[col];
+    for (int i = 0; i < kc; ++i) v = fma(h.coef[static_cast<size_t>(i) * h.bpad + col], h.slots[i * h.slot + e], v);
+    return v;
+}
+
+// c_i per column from the recorded a_k, beta_k; kcol = min(iterations, limit)
+static __global__ void cg_hist_coef_kernel(const double* __restrict__ ahist, const double* __restrict__ bhist,
+                                           const int64_t* __restrict__ iters, int limit, int b, int bpad,
+                                           double* __restrict__ coef, int32_t* __restrict__ kcol) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= bpad) return;
+    const int k = col < b ? static_cast<int>(iters[col] < limit ? iters[col] : limit) : 0;
+    kcol[col] = k;
+    double c = 0.0;
+    for (int i = k - 1; i >= 0; --i) {
+        c = fma(bhist[static_cast<size_t>(i) * bpad + col], c, ahist[static_cast<size_t>(i) * bpad + col]);
+        coef[static_cast<size_t>(i) * bpad + col] = c;
+    }
+}
+
+// x = x_0 + sum_i c_i r_i over the whole chunked block (the fold)
+template <int C>
+__global__ void cg_hist_fold_kernel(double* __restrict__ x, CgHistory h, int64_t rows, int nchunks) {
+    const size_t total = static_cast<size_t>(nchunks) * rows * C;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(e % C);
+        const int chunk = static_cast<int>(e / (static_cast<size_t>(rows) * C));
+        x[e] = hist_value(h, e, chunk * C + c);
     }
 }
 
@@ -423,7 +502,7 @@ __global__ void load_colmajor_kernel(double* __restrict__ dst, const double* __r
 template <int C>
 __global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __restrict__ src,
                                       int64_t rows, int64_t ld, int b, int nchunks,
-                                      const int64_t* __restrict__ perm, int clamp) {
+                                      const int64_t* __restrict__ perm, int clamp, CgHistory hist = CgHistory()) {
     constexpr int TR = 64;
     __shared__ double sm[TR * (C + 1)];
     const int64_t ntiles = (rows + TR - 1) / TR;
@@ -433,7 +512,8 @@ __global__ void store_colmajor_kernel(double* __restrict__ dst, const double* __
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
             const int rr = e / C, c = e % C;
             const int64_t row = r0 + rr;
-            sm[rr * (C + 1) + c] = row < rows ? src[static_cast<size_t>(chunk) * ld + static_cast<size_t>(row) * C + c] : 0.0;
+            const size_t e2 = static_cast<size_t>(chunk) * ld + static_cast<size_t>(row < rows ? row : 0) * C + c;
+            sm[rr * (C + 1) + c] = row < rows ? (hist.kcol ? hist_value(hist, e2, chunk * C + c) : src[e2]) : 0.0;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
@@ -465,7 +545,7 @@ static __global__ void invert_perm_kernel(const int64_t* __restrict__ perm, int6
 template <int C>
 __global__ void store_gather_kernel(double* __restrict__ dst, const double* __restrict__ src,
                                     int64_t rows, int64_t ld, int b, int nchunks,
-                                    const int64_t* __restrict__ iperm, int clamp) {
+                                    const int64_t* __restrict__ iperm, int clamp, CgHistory hist = CgHistory()) {
     constexpr int TR = 64;
     __shared__ double sm[TR * (C + 1)];
     const int64_t ntiles = (rows + TR - 1) / TR;
@@ -475,8 +555,8 @@ __global__ void store_gather_kernel(double* __restrict__ dst, const double* __re
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
             const int rr = e / C, c = e % C;
             const int64_t row = r0 + rr;
-            sm[rr * (C + 1) + c] =
-                row < rows ? src[static_cast<size_t>(chunk) * ld + static_cast<size_t>(iperm[row]) * C + c] : 0.0;
+            const size_t e2 = static_cast<size_t>(chunk) * ld + static_cast<size_t>(row < rows ? iperm[row] : 0) * C + c;
+            sm[rr * (C + 1) + c] = row < rows ? (hist.kcol ? hist_value(hist, e2, chunk * C + c) : src[e2]) : 0.0;
         }
         __syncthreads();
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {

@@ -32,7 +32,10 @@ namespace {
 
 struct CgWork {
     int C, nchunks, bpad, nb;
-    double *x, *r, *p, *q;
+    int H = 0;             // residual-history slots (0: x updated every iteration)
+    double *x, *r, *p, *q; // r = slot 0 of the H residual slots
+    double *ahist = nullptr, *bhist = nullptr, *coef = nullptr;  // [H][bpad]
+    int32_t* kcol = nullptr;                                     // [bpad]
     SpmmScratch sp;
     RedScratch red;
     SolveState st;
@@ -47,10 +50,25 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.bpad = w.nchunks * w.C;
     w.nb = stream_ctas_per_chunk(g->rows, w.C, w.nchunks);
     const size_t blk = static_cast<size_t>(w.bpad) * g->rows;
+    // residual-history slots (see blockops.cuh CgHistory): up to
+    // KZ_CG_HISTORY (default 8) while the vector blocks stay under 64 GB
+    {
+        const char* e = std::getenv("KZ_CG_HISTORY");
+        const int want = e ? std::atoi(e) : 8;
+        const double blk_gb = static_cast<double>(blk) * 8.0 / 1e9;
+        int h = static_cast<int>(std::min<double>(want, std::floor(64.0 / std::max(blk_gb, 1e-9)) - 3.0));
+        w.H = h >= 3 ? h : 0;
+    }
     w.x = cv.take<double>(blk);
-    w.r = cv.take<double>(blk);
+    w.r = cv.take<double>(blk * static_cast<size_t>(std::max(1, w.H)));
     w.p = cv.take<double>(blk);
     w.q = cv.take<double>(blk);
+    if (w.H) {
+        w.ahist = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
+        w.bhist = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
+        w.coef = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
+        w.kcol = cv.take<int32_t>(w.bpad);
+    }
     carve_spmm_scratch(cv, g, w.nchunks, w.C, w.sp);
     w.red.nb = w.nb;
     w.red.part = cv.take<double>(static_cast<size_t>(w.nchunks) * w.nb * w.C);
@@ -134,8 +152,21 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     KZ_CUDA(cudaMemsetAsync(s.rs, 0, reinterpret_cast<char*>(w.qpos) - reinterpret_cast<char*>(s.rs), st));
     KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nchunks, st));
     if (int rc = zero_spmm_counters(g, nchunks, w.sp, st)) return rc;
-    const size_t blk_bytes = sizeof(double) * static_cast<size_t>(w.bpad) * n;
-    if (!eig) KZ_CUDA(cudaMemsetAsync(w.x, 0, blk_bytes, st));  // the eigen start writes every x
+    const size_t blk_elems = static_cast<size_t>(w.bpad) * n;
+    const size_t blk_bytes = sizeof(double) * blk_elems;
+    const double work = static_cast<double>(g->nnz + n) * w.bpad;
+    const bool use_graphs = work <= kGraphWork && graphs_enabled();
+    // residual-history mode (blockops.cuh CgHistory): x is formed at the end
+    // from the kept residuals instead of being updated every iteration
+    const bool hist = w.H >= 3 && !use_graphs;
+    const bool has_x0 = eig != nullptr || a->x0 != nullptr;
+    if (hist) {
+        KZ_CUDA(cudaMemsetAsync(w.ahist, 0, sizeof(double) * static_cast<size_t>(w.H) * w.bpad, st));
+        KZ_CUDA(cudaMemsetAsync(w.bhist, 0, sizeof(double) * static_cast<size_t>(w.H) * w.bpad, st));
+    }
+    // x0 = 0: the eigen start writes every x, a seeded start broadcasts it,
+    // and the history form never reads an x it did not write
+    if (!has_x0 && !hist) KZ_CUDA(cudaMemsetAsync(w.x, 0, blk_bytes, st));
 
     const unsigned sgrid = static_cast<unsigned>(nchunks) * nb;
     const unsigned tgrid = static_cast<unsigned>(std::min<int64_t>(
@@ -226,9 +257,26 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     }
     if (!eig) KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));  // p0 = r0
 
-    const double work = static_cast<double>(g->nnz + n) * w.bpad;
     const int lag = work > 2e7 ? 1 : 3;
-    const bool use_graphs = work <= kGraphWork && graphs_enabled();
+    auto slot = [&](int i) { return w.r + static_cast<size_t>(i) * blk_elems; };
+    auto history = [&]() {
+        CgHistory h;
+        h.slots = w.r;
+        h.slot = blk_elems;
+        h.coef = w.coef;
+        h.kcol = w.kcol;
+        h.x0 = has_x0 ? w.x : nullptr;
+        h.bpad = w.bpad;
+        return h;
+    };
+    auto hist_coef = [&](int limit) -> int {
+        cg_hist_coef_kernel<<<static_cast<unsigned>((w.bpad + 127) / 128), 128, 0, st>>>(
+            w.ahist, w.bhist, s.iters, limit, b, w.bpad, w.coef, w.kcol);
+        ::kz::note_launch();
+        KZ_LAUNCH_CHECK();
+        return KZ_OK;
+    };
+    bool folded = false;
     // a solve from zero with b = beta A e_q: the first iteration's SpMM is
     // replaced by the 2-walk counts (cg_sparse_pq_kernel); KZ_CG_SPARSE_FIRST=0
     // turns it off
@@ -237,6 +285,22 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs &&
                               w.bpad <= 65535;  // one grid row per column in walk2_count_kernel
     auto launch_iter = [&](int k) -> int {
+        // history mode for iterations 1 .. H-1: r_k -> slot k, no x update;
+        // a solve that needs iteration H folds x once and continues in place
+        if (hist && !folded && k >= w.H) {
+            if (int rc = hist_coef(w.H - 1)) return rc;
+            const unsigned fgrid = static_cast<unsigned>(std::min<int64_t>(8 * kMaxCtasPerChunk, (static_cast<int64_t>(blk_elems) + 255) / 256));
+            KZ_DISPATCH_C(C, cg_hist_fold_kernel<CC><<<fgrid, 256, 0, st>>>(w.x, history(), n, nchunks); ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            folded = true;
+        }
+        const bool hmode = hist && !folded;
+        double* rin = hist ? (folded ? slot(w.H - 1) : slot(k - 1)) : w.r;
+        double* rout = hmode ? slot(k) : nullptr;
+        double* rcur = hmode ? rout : rin;  // r_k after this iteration's update
+        double* xk = hmode ? nullptr : w.x;
+        double* ah = hmode ? w.ahist + static_cast<size_t>(k - 1) * w.bpad : nullptr;
+        double* bh = hmode ? w.bhist + static_cast<size_t>(k - 1) * w.bpad : nullptr;
         if (k == 1 && sparse_first) {
             int32_t* cnt = reinterpret_cast<int32_t*>(w.q);
             KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
@@ -246,15 +310,15 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                                                                                 w.qpos, b);
                           ::kz::note_launch());
             KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_sparse_pq_kernel<CC><<<w.bpad, kThreads, 0, st>>>(w.r, cnt, n * CC, g->rowptr,
+            KZ_DISPATCH_C(C, cg_sparse_pq_kernel<CC><<<w.bpad, kThreads, 0, st>>>(rin, cnt, n * CC, g->rowptr,
                                                                                   g->colidx, w.qpos, a->beta, s, k);
                           ::kz::note_launch());
             KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, n * CC, n * CC, w.red,
-                                                                              FIN_CG_CONV, s, k, cnt, a->beta);
+            KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red,
+                                                                              FIN_CG_CONV, s, k, cnt, a->beta, rout);
                           ::kz::note_launch());
             KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, w.r, n, n * CC, n * CC, n * CC, nb, s, k); ::kz::note_launch());
+            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh); ::kz::note_launch());
             KZ_LAUNCH_CHECK();
             return KZ_OK;
         }
@@ -282,9 +346,9 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         sa.hook.iter = k;
         sa.hook.iter_dev = s.iter_dev;
         if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
-        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k); ::kz::note_launch());
+        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k, nullptr, 0.0, rout); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
-        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, w.r, n, n * CC, n * CC, n * CC, nb, s, k); ::kz::note_launch());
+        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
         return KZ_OK;
     };
@@ -294,12 +358,18 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                         : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
     if (rc) return rc;
 
+    // the output pass forms x from the residual history unless it was folded
+    CgHistory oh;
+    if (hist && !folded) {
+        if (int rc2 = hist_coef(w.H)) return rc2;
+        oh = history();
+    }
     if (a->perm) {
         invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
         ::kz::note_launch();
-        KZ_DISPATCH_C(C, store_gather_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, w.iperm, a->clamp); ::kz::note_launch());
+        KZ_DISPATCH_C(C, store_gather_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, w.iperm, a->clamp, oh); ::kz::note_launch());
     } else {
-        KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, nullptr, a->clamp); ::kz::note_launch());
+        KZ_DISPATCH_C(C, store_colmajor_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, nullptr, a->clamp, oh); ::kz::note_launch());
     }
     KZ_LAUNCH_CHECK();
     if (a->device_ms) {
