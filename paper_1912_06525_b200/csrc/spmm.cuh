@@ -43,10 +43,19 @@
 #include "common.cuh"
 
 namespace kz {
-constexpr int kMedDeg = 32;      // rows with deg <= kMedDeg are "short"
-constexpr int kSegLen = 1024;    // rows with deg > kSegLen are split into segments
+#ifndef KZ_K1_MEDDEG
+#define KZ_K1_MEDDEG 32
+#endif
+#ifndef KZ_K1_SEGLEN
+#define KZ_K1_SEGLEN 4096
+#endif
+#ifndef KZ_K1_GROUPCOST
+#define KZ_K1_GROUPCOST 4096.0
+#endif
+constexpr int kMedDeg = KZ_K1_MEDDEG;    // rows with deg <= kMedDeg are "short"
+constexpr int kSegLen = KZ_K1_SEGLEN;    // rows with deg > kSegLen are split into segments
 constexpr int kGroupTasks = 8;   // max tasks a warp dequeues at once (one dot slot)
-constexpr double kGroupCost = 1024.0;  // max neighbour-equivalents per work unit
+constexpr double kGroupCost = KZ_K1_GROUPCOST;  // max neighbour-equivalents per work unit
 constexpr int kSuperGroups = 256; // max groups reduced together by their last finisher
 #ifndef KZ_K1_MINBLOCKS
 #define KZ_K1_MINBLOCKS 5  // resident CTAs per SM the register budget is sized for
