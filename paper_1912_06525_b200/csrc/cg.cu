@@ -56,7 +56,8 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
         const char* e = std::getenv("KZ_CG_HISTORY");
         const int want = e ? std::atoi(e) : 8;
         const double blk_gb = static_cast<double>(blk) * 8.0 / 1e9;
-        int h = static_cast<int>(std::min<double>(want, std::floor(64.0 / std::max(blk_gb, 1e-9)) - 3.0));
+        int h = static_cast<int>(std::min<double>(std::min(want, kMaxHist),
+                                                  std::floor(64.0 / std::max(blk_gb, 1e-9)) - 3.0));
         w.H = h >= 3 ? h : 0;
     }
     w.x = cv.take<double>(blk);

@@ -97,7 +97,10 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, 
     const double est_total = static_cast<double>(rp[rows]) + 4.0 * static_cast<double>(rows);
     const double unit = std::max(64.0, std::min(kGroupCost, est_total / (2.0 * kNumSMs * kSpmmMinBlocks * kWarps)));
     const int s_rows_max = unit >= 512.0 ? 32 : (unit >= 128.0 ? 8 : 4);
-    const double s_cost_max = std::min(256.0, unit);
+#ifndef KZ_K1_SCOST
+#define KZ_K1_SCOST 256.0
+#endif
+    const double s_cost_max = std::min(KZ_K1_SCOST, unit);
     std::vector<int64_t> long_rows;  // blocked: rows deferred to the block phases
     for (int64_t i = 0; i < rows; ++i) {
         const int64_t d = rp[i + 1] - rp[i];

@@ -54,7 +54,10 @@ namespace kz {
 #endif
 constexpr int kMedDeg = KZ_K1_MEDDEG;    // rows with deg <= kMedDeg are "short"
 constexpr int kSegLen = KZ_K1_SEGLEN;    // rows with deg > kSegLen are split into segments
-constexpr int kGroupTasks = 8;   // max tasks a warp dequeues at once (one dot slot)
+#ifndef KZ_K1_GROUPTASKS
+#define KZ_K1_GROUPTASKS 8
+#endif
+constexpr int kGroupTasks = KZ_K1_GROUPTASKS;   // max tasks a warp dequeues at once (one dot slot)
 constexpr double kGroupCost = KZ_K1_GROUPCOST;  // max neighbour-equivalents per work unit
 constexpr int kSuperGroups = 256; // max groups reduced together by their last finisher
 #ifndef KZ_K1_MINBLOCKS
