@@ -21,6 +21,7 @@ ap.add_argument("--b", type=int, default=256)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--settings", default="0:128:1,16:128:1,32:128:1,48:128:1,32:64:1,32:1024:1,32:128:0")
 ap.add_argument("--out", default=None)
+ap.add_argument("--chunk", type=int, default=32)
 a = ap.parse_args()
 
 g = G.rmat_graph_fast(a.scale)
@@ -28,7 +29,7 @@ order = rcm_order(g)
 inv = np.empty(g.n, dtype=np.int64)
 inv[order] = np.arange(g.n)
 off, col = permute_csr(g.row_offsets, g.col_indices, order, inv)
-n, b, C = g.n, a.b, 32
+n, b, C = g.n, a.b, a.chunk
 torch.manual_seed(0)
 X = torch.randn(b * n, dtype=torch.float64, device="cuda")
 Y = torch.empty_like(X)
