@@ -110,8 +110,8 @@ struct Cfg {
     static constexpr int SVEC = (C >= 2) ? 2 : 1;  // doubles per lane of the streaming kernels
     static constexpr int G = C / VEC;             // lanes per row group
     static constexpr int NGW = 32 / G;            // row groups per warp
-    // neighbours gathered per round: 8 (4 for narrow groups) -- R*VEC doubles
-    // of gather registers per lane
+    // neighbours gathered per round: 8 with 16-byte loads, 4 with 32-byte loads (4 for
+    // narrow groups) -- R*VEC doubles of gather registers per lane either way
     static constexpr int R = (C >= 32 && KZ_K1_R32 > 0) ? KZ_K1_R32 : ((G >= 8) ? (VEC == 4 ? 4 : 8) : (G >= 4 ? G : 4));
     static constexpr int PER = (R >= G) ? R / G : 1;  // indices loaded per lane per round
     static constexpr bool PART = R < G;               // only lanes lg < R load indices
