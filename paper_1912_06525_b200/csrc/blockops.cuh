@@ -329,7 +329,8 @@ template <int C>
 __global__ void __launch_bounds__(kThreads)
     cg_pupdate_kernel(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ d,
                       int64_t rows, int64_t ldx, int64_t ldp, int64_t ldd, int nb, SolveState s,
-                      int iter, double* __restrict__ ahist = nullptr, double* __restrict__ bhist = nullptr) {
+                      int iter, double* __restrict__ ahist = nullptr, double* __restrict__ bhist = nullptr,
+                      const double* __restrict__ p_in = nullptr) {
     constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / nb, local = blockIdx.x - chunk * nb;
     iter = cur_iter(s, iter);
@@ -346,6 +347,9 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
     if (x) x += static_cast<size_t>(chunk) * ldx;
+    // p_in: the previous direction when it is not in p (history mode, first
+    // iteration: p_0 = r_0 lives in residual slot 0)
+    const double* __restrict__ pi_ = (p_in ? p_in : p) + static_cast<size_t>(chunk) * ldp;
     p += static_cast<size_t>(chunk) * ldp;
     d += static_cast<size_t>(chunk) * ldd;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
@@ -381,7 +385,7 @@ __global__ void __launch_bounds__(kThreads)
         // history mode: p = d + betac*p only (3 block passes)
         for (size_t pi = t0; pi < npairs; pi += stride) {
             double pv[VEC], dv[VEC];
-            ld_plain<VEC>(p + pi * VEC, pv);
+            ld_plain<VEC>(pi_ + pi * VEC, pv);
             ld_plain<VEC>(d + pi * VEC, dv);
 #pragma unroll
             for (int k = 0; k < VEC; ++k)

@@ -235,7 +235,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_DISPATCH_C(C, {                                                                                     \
             KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                          static_cast<int>(smem)));                                             \
-            lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, w.p, n * CC, \
+            lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, hist ? nullptr : w.p, n * CC, \
                                                                             j0, w.bpad, cnt);                  \
             ::kz::note_launch();                                                                               \
         });                                                                                                    \
@@ -248,7 +248,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
             KZ_LAUNCH_CHECK();
         }
         // b = beta A e_q onto r0 and p0, or (walk start) onto x0
-        KZ_DISPATCH_C(C, eigen_add_rhs_kernel<CC><<<w.bpad, kThreads, 0, st>>>(cnt ? w.x : w.r, cnt ? nullptr : w.p,
+        KZ_DISPATCH_C(C, eigen_add_rhs_kernel<CC><<<w.bpad, kThreads, 0, st>>>(cnt ? w.x : w.r, cnt || hist ? nullptr : w.p,
                                                                                 n * CC, g->rowptr, g->colidx,
                                                                                 w.qpos, b, a->beta, s.bnorm2);
                       ::kz::note_launch());
@@ -256,7 +256,9 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
     }
-    if (!eig) KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));  // p0 = r0
+    // p0 = r0; in history mode r0 stays in slot 0, so the first iteration reads
+    // its direction from there and p is first written by that pupdate
+    if (!eig && !hist) KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));
 
     const int lag = work > 2e7 ? 1 : 3;
     auto slot = [&](int i) { return w.r + static_cast<size_t>(i) * blk_elems; };
@@ -319,13 +321,14 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                                                                               FIN_CG_CONV, s, k, cnt, a->beta, rout);
                           ::kz::note_launch());
             KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh); ::kz::note_launch());
+            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh, hmode ? rin : nullptr); ::kz::note_launch());
             KZ_LAUNCH_CHECK();
             return KZ_OK;
         }
+        const double* pin = hmode && k == 1 ? rin : w.p;  // p_0 = r_0 (slot 0) in history mode
         SpmmArgs sa = make_spmm_args(g, w.sp);
-        sa.Xg = w.p;
-        sa.Xs = w.p;
+        sa.Xg = pin;
+        sa.Xs = pin;
         sa.Z = nullptr;
         sa.Y = w.q;
         sa.s0 = 0.0;
@@ -349,7 +352,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
         KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k, nullptr, 0.0, rout); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
-        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh); ::kz::note_launch());
+        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh, pin != w.p ? pin : nullptr); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
         return KZ_OK;
     };

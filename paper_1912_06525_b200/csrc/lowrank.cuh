@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
                         if (c) r0 = __dadd_rn(r0, __dmul_rn(__dmul_rn(h.beta, h.beta), static_cast<double>(c)));
                     }
                     r[off] = r0;
-                    p[off] = r0;
+                    if (p) p[off] = r0;
                 }
         }
     }
