@@ -90,12 +90,16 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, 
         }
     };
     const bool blocked = o.nblocks > 1 && col != nullptr && cols > 0;
-    const int64_t min_deg = blocked ? std::min<int64_t>(std::max<int64_t>(o.min_deg, kMedDeg), kSegLen) : kSegLen;
     int32_t nlong = 0, nseg = 0;
     max_deg = 0;
     // granularity: aim for >= ~2 work units per resident warp of one chunk pass
     const double est_total = static_cast<double>(rp[rows]) + 4.0 * static_cast<double>(rows);
     const double unit = std::max(64.0, std::min(kGroupCost, est_total / (2.0 * kNumSMs * kSpmmMinBlocks * kWarps)));
+    // hub segments no longer than a work unit (at least 1,024): large
+    // operators get kSegLen, small ones keep short segments so one hub row
+    // does not become a serial tail
+    const int64_t seglen = std::max<int64_t>(1024, std::min<int64_t>(kSegLen, static_cast<int64_t>(unit)));
+    const int64_t min_deg = blocked ? std::min<int64_t>(std::max<int64_t>(o.min_deg, kMedDeg), seglen) : seglen;
     const int s_rows_max = unit >= 512.0 ? 32 : (unit >= 128.0 ? 8 : 4);
 #ifndef KZ_K1_SCOST
 #define KZ_K1_SCOST 256.0
@@ -125,8 +129,8 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, 
             close_s(i);
             long_seg0.push_back(nseg);
             int k = 0;
-            for (int64_t p = rp[i]; p < rp[i + 1]; p += kSegLen, ++k) {
-                const int64_t e = std::min<int64_t>(p + kSegLen, rp[i + 1]);
+            for (int64_t p = rp[i]; p < rp[i + 1]; p += seglen, ++k) {
+                const int64_t e = std::min<int64_t>(p + seglen, rp[i + 1]);
                 tasks.push_back(make_int4(static_cast<int>(i), nlong, TASK_L, k));
                 cost.push_back(static_cast<double>(e - p) + 8.0);
                 seg_range.push_back(make_int2(static_cast<int>(p), static_cast<int>(e)));
@@ -164,7 +168,7 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, 
         for (size_t l = 0; l < nl; ++l) {
             int64_t ns = 0;
             for (int k = 0; k < K; ++k)
-                ns += (bstart[l * (K + 1) + k + 1] - bstart[l * (K + 1) + k] + kSegLen - 1) / kSegLen;
+                ns += (bstart[l * (K + 1) + k + 1] - bstart[l * (K + 1) + k] + seglen - 1) / seglen;
             seg0[l + 1] = seg0[l] + static_cast<int32_t>(ns);
         }
         long_seg0.assign(seg0.begin(), seg0.end());
@@ -185,9 +189,9 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, 
             }
             for (size_t l = 0; l < nl; ++l) {
                 const int64_t i = long_rows[l], e = bstart[l * (K + 1) + k + 1];
-                for (int64_t p = bstart[l * (K + 1) + k]; p < e; p += kSegLen) {
+                for (int64_t p = bstart[l * (K + 1) + k]; p < e; p += seglen) {
                     const int kk = next[l]++;
-                    const int64_t pe = std::min<int64_t>(p + kSegLen, e);
+                    const int64_t pe = std::min<int64_t>(p + seglen, e);
                     tasks.push_back(make_int4(static_cast<int>(i), static_cast<int>(l), TASK_L, kk));
                     cost.push_back(static_cast<double>(pe - p) + 8.0);
                     seg_range[seg0[l] + kk] = make_int2(static_cast<int>(p), static_cast<int>(pe));
