@@ -399,6 +399,8 @@ template <int C, bool W>
 __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs a) {
     using K = Cfg<C>;
     constexpr int VEC = K::VEC;
+    constexpr bool SD = (KZ_K1_SMEM_DOT != 0) && C >= 32;
+    __shared__ double s_dacc[SD ? VEC * kThreads : 1];
     const int lane = threadIdx.x & 31;
     const int gw = lane / K::G, lg = lane % K::G, gbase = gw * K::G;
     const unsigned gmask = (K::G == 32) ? 0xffffffffu : (((1u << K::G) - 1u) << gbase);
@@ -412,17 +414,17 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         const int chunk = g / a.ngroups, gl = g - chunk * a.ngroups;
         if (a.chunk_active && !a.chunk_active[chunk]) continue;
         const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.ldxg;
-#if KZ_K1_SMEM_DOT
-        // the column-dot accumulators live in shared memory (one slot per
-        // thread), not in registers across the gather loop
-        __shared__ double s_dacc[VEC * kThreads];
+        // wide chunks (32-byte gathers): the column-dot accumulators live in
+        // shared memory (one slot per thread), not in registers across the
+        // gather loop; narrow chunks keep them in registers
+        double dacc_r[VEC];
+        if constexpr (SD) {
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) s_dacc[q * kThreads + threadIdx.x] = 0.0;
-#else
-        double dacc[VEC];
+            for (int q = 0; q < VEC; ++q) s_dacc[q * kThreads + threadIdx.x] = 0.0;
+        } else {
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) dacc[q] = 0.0;
-#endif
+            for (int q = 0; q < VEC; ++q) dacc_r[q] = 0.0;
+        }
 
         auto epilogue = [&](int row, const double (&acc)[VEC]) {
             const size_t roff = static_cast<size_t>(row) * C + lg * VEC;
@@ -450,12 +452,12 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
                                   : a.Xs + static_cast<size_t>(chunk) * a.ldxs + roff, d);
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) {
-#if KZ_K1_SMEM_DOT
-                    double& da = s_dacc[q * kThreads + threadIdx.x];
-                    da = fma(d[q], y[q], da);
-#else
-                    dacc[q] = fma(d[q], y[q], dacc[q]);
-#endif
+                    if constexpr (SD) {
+                        double& da = s_dacc[q * kThreads + threadIdx.x];
+                        da = fma(d[q], y[q], da);
+                    } else {
+                        dacc_r[q] = fma(d[q], y[q], dacc_r[q]);
+                    }
                 }
             }
         };
@@ -535,11 +537,9 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         if (!a.want_dot) continue;
 
         // ---- deterministic dot reduction: group -> super group -> chunk ----
-#if KZ_K1_SMEM_DOT
         double dacc[VEC];
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) dacc[q] = s_dacc[q * kThreads + threadIdx.x];
-#endif
+        for (int q = 0; q < VEC; ++q) dacc[q] = SD ? s_dacc[q * kThreads + threadIdx.x] : dacc_r[q];
         warp_sum(dacc);
         double* gs = a.gslot + (static_cast<size_t>(chunk) * a.ngroups + gl) * C;
         if (lane < K::G) {
