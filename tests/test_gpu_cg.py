@@ -259,6 +259,30 @@ def test_cg_sparse_first_iteration_matches_dense(torch, kz, cfg, monkeypatch):
     assert np.all(diff <= 1e-12), diff.max()
 
 
+@pytest.mark.parametrize("tol", [1e-8, 1e-12])
+def test_cg_residual_history_matches_per_iteration_update(torch, kz, monkeypatch, tol):
+    """The residual-history form of the solution (x = x0 + sum c_i r_i,
+    blockops.cuh CgHistory; folded into x when a solve outgrows its slots,
+    which tol 1e-12 forces) against the per-iteration x update
+    (KZ_CG_HISTORY=0): identical iteration counts, scores within roundoff,
+    for plain CG and the eigen form."""
+    from paper_1912_06525_b200.generators import CONFIGS, config_graph, sample_queries
+
+    g = config_graph("proxy16")
+    lam = kz.spectral_norm(g)
+    gi = kz.GraphIndex(g, 0.5 / lam)
+    ei = kz.EigenIndex(gi, 16)
+    qs = sample_queries(g.original_ids, 40, seed=2)
+    for fn, idx in ((kz.query_cg_baseline_batch, gi), (kz.query_batch, ei)):
+        s1, r1 = fn(idx, qs, tol=tol, device=True)
+        monkeypatch.setenv("KZ_CG_HISTORY", "0")
+        s0, r0 = fn(idx, qs, tol=tol, device=True)
+        monkeypatch.delenv("KZ_CG_HISTORY")
+        assert [r.iterations for r in r1] == [r.iterations for r in r0]
+        diff = (torch.linalg.vector_norm(s1 - s0, dim=1) / torch.linalg.vector_norm(s0, dim=1)).cpu().numpy()
+        assert np.all(diff <= 1e-13), diff.max()
+
+
 def test_topk_matches_lexsort(torch, kz):
     rng = np.random.default_rng(4)
     b, n = 7, 50_000
