@@ -348,6 +348,11 @@ def main():
                          "gathered_tbs": 8.0 * nnz * b / (spmm_ms / 1e3) / 1e12,
                          "algorithmic_bytes_per_launch": b_spmm, "launch_ms": spmm_ms,
                          "peak_source": peak_src,
+                         "note": ("K1 gathers 8*nnz*b bytes per launch through L2 (gathered_tbs); the measured "
+                                  "random 256-byte-row gather ceilings of this part are ~20 TB/s L2-resident and "
+                                  "~7.7 TB/s at K1's 612 MB chunk working set (profiles/r01_tma_gather_microbench.json, "
+                                  "r01_l2bw.json); dram_traffic_frac is ncu's DRAM bytes per launch over this run's "
+                                  "launch time"),
                          "cg_iteration": {"algorithmic_bytes": b_cg, "ms": cg_iter_ms,
                                           "achieved_gbs": b_cg / (cg_iter_ms / 1e3) / 1e9,
                                           "note": "solve time per step / max iterations"
