@@ -50,8 +50,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solver", default="eigen", choices=["eigen", "cg"])
-    ap.add_argument("--walk-terms", type=int, default=1, choices=[0, 1],
-                    help="eigen start: 1 = first Katz term exact + Galerkin on the remainder")
+    ap.add_argument("--walk-terms", type=int, default=2, choices=[0, 1, 2],
+                    help="eigen start: Katz-series terms put in exactly before the Galerkin step (0, 1, 2)")
     return ap.parse_args()
 
 
@@ -329,7 +329,8 @@ def main():
                        "queries_per_gpu": b, "top_k": k, "tol": tol,
                        "solver": (f"LRC-Katz, eigen form: rank-{eidx.rank} eigen index of A (low-rank Galerkin "
                                   f"term, two fp64 DMMA GEMMs"
-                                  + (", first Katz term beta*A*e_q exact via 2-walk counts" if eidx.walk_terms else "")
+                                  + ({0: "", 1: ", first Katz term beta*A*e_q exact via 2-walk counts",
+                                      2: ", first two Katz terms exact (2-walk counts), r0 from one SpMM"}[eidx.walk_terms])
                                   + ") + CG correction" if eidx is not None
                                   else "plain CG (query_cg_baseline)"),
                        "eigen_index_build_s": round(t_index, 2) if eidx is not None else None,

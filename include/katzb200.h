@@ -228,7 +228,10 @@ int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const in
  * With a2u = A^2 U (optional) the start also carries the first Katz-series
  * term exactly: x0 = beta A e_q + U y, y = beta^2 W (A^2 U)[q,:]', whose
  * residual r0 = beta^2 A^2 e_q - U y + beta (AU) y needs only the 2-walk
- * counts from q (an integer sparse push, no SpMM): one CG iteration fewer. */
+ * counts from q (an integer sparse push, no SpMM): one CG iteration fewer.
+ * With a3u = A^3 U the start carries the first two terms, x0 = beta A e_q +
+ * beta^2 A^2 e_q + U y, y = beta^3 W (A^3 U)[q,:]', and r0 comes from one
+ * SpMM on x0 (no (AU) y product): one more CG iteration fewer. */
 typedef struct kz_eigen kz_eigen;
 typedef struct kz_eigen_desc {
     int64_t n, r;
@@ -239,6 +242,7 @@ typedef struct kz_eigen_desc {
     const double* au;     /* device n x ldr row-major, A U */
     const double* w;      /* device r x r row-major, (I - beta U'AU)^-1 */
     const double* a2u;    /* device n x ldr row-major, A^2 U; NULL: plain Galerkin start */
+    const double* a3u;    /* device n x ldr row-major, A^3 U: two-term walk start (takes precedence) */
 } kz_eigen_desc;
 int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out);
 int kz_eigen_destroy(kz_eigen* h);

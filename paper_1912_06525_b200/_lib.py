@@ -132,6 +132,7 @@ class KzEigenDesc(ctypes.Structure):
         ("au", ctypes.c_void_p),
         ("w", ctypes.c_void_p),
         ("a2u", ctypes.c_void_p),
+        ("a3u", ctypes.c_void_p),
     ]
 
 

@@ -217,7 +217,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         const size_t smem = lowrank_smem(eig->ldr, 8 * nt);
         // walk start: 2-walk counts into the (still unused) q block, int32
         int32_t* cnt = nullptr;
-        if (eig->a2u) {
+        const bool two_term = eig->a3u != nullptr;
+        if (eig->a2u || two_term) {
             cnt = reinterpret_cast<int32_t*>(w.q);
             KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
             const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, g->max_deg))),
@@ -233,10 +234,17 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
 #define KZ_LR(NN)                                                                                              \
     do {                                                                                                       \
         KZ_DISPATCH_C(C, {                                                                                     \
-            KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         static_cast<int>(smem)));                                             \
-            lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, hist ? nullptr : w.p, n * CC, \
-                                                                            j0, w.bpad, cnt);                  \
+            if (two_term) {                                                                                    \
+                KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN, true>,                                \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
+                lowrank_init_kernel<CC, NN, true><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, nullptr, \
+                                                                                      nullptr, n * CC, j0, w.bpad, cnt); \
+            } else {                                                                                           \
+                KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             static_cast<int>(smem)));                                         \
+                lowrank_init_kernel<CC, NN><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, w.r, hist ? nullptr : w.p, n * CC, \
+                                                                                j0, w.bpad, cnt);              \
+            }                                                                                                  \
             ::kz::note_launch();                                                                               \
         });                                                                                                    \
     } while (0)
@@ -253,6 +261,27 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                                                                                 w.qpos, b, a->beta, s.bnorm2);
                       ::kz::note_launch());
         KZ_LAUNCH_CHECK();
+        if (two_term) {
+            // r0 = b - (x0 - beta A x0): one K1 SpMM on x0 (exactly consistent
+            // with x0), then the rhs scattered on top
+            SpmmArgs sa = make_spmm_args(g, w.sp);
+            sa.Xg = w.x;
+            sa.Xs = w.x;
+            sa.Z = nullptr;
+            sa.Y = w.r;
+            sa.s0 = 0.0;
+            sa.s1 = -1.0;
+            sa.s2 = a->beta;
+            sa.want_dot = 0;
+            sa.chunk_active = nullptr;
+            if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
+            KZ_DISPATCH_C(C, eigen_add_rhs_kernel<CC><<<w.bpad, kThreads, 0, st>>>(w.r, nullptr, n * CC, g->rowptr,
+                                                                                    g->colidx, w.qpos, b, a->beta,
+                                                                                    s.bnorm2);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            if (!hist) KZ_CUDA(cudaMemcpyAsync(w.p, w.r, blk_bytes, cudaMemcpyDeviceToDevice, st));
+        }
         KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red, FIN_INIT_R, s, nullptr, 0); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
     }
@@ -432,6 +461,7 @@ extern "C" int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out) {
     h->au = d->au;
     h->w = d->w;
     h->a2u = d->a2u;
+    h->a3u = d->a3u;
     *out = h;
     return KZ_OK;
 }

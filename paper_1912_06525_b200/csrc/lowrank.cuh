@@ -35,6 +35,7 @@ struct kz_eigen {
     const double* au = nullptr;     // device n x ldr row-major
     const double* w = nullptr;      // device r x r row-major, symmetric
     const double* a2u = nullptr;    // optional device n x ldr row-major, A^2 U (walk start)
+    const double* a3u = nullptr;    // optional device n x ldr row-major, A^3 U (two-term walk start)
 };
 
 namespace kz {
@@ -49,10 +50,11 @@ __global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos
     if (k >= h.ldr) return;
     double s = 0.0;
     if (j < b && k < h.r) {
-        const double* __restrict__ aurow = (h.a2u ? h.a2u : h.au) + qpos[j] * h.ldr;
+        const double* __restrict__ aurow = (h.a3u ? h.a3u : h.a2u ? h.a2u : h.au) + qpos[j] * h.ldr;
         const double* __restrict__ wrow = h.w + k * h.r;
         for (int64_t i = 0; i < h.r; ++i) s = fma(wrow[i], __ldg(aurow + i), s);
-        s *= h.a2u ? __dmul_rn(h.beta, h.beta) : h.beta;
+        const double b2 = __dmul_rn(h.beta, h.beta);
+        s *= h.a3u ? __dmul_rn(b2, h.beta) : h.a2u ? b2 : h.beta;
     }
     y[static_cast<size_t>(j / C) * h.ldr * C + static_cast<size_t>(k) * C + (j % C)] = s;
 }
@@ -83,7 +85,9 @@ __device__ __forceinline__ void lr_dmma(double& d0, double& d1, double a, double
 // y's group columns are staged in shared memory once per CTA ([ldr][NC+8],
 // bank padded); each warp owns 16 rows of a 128-row tile and streams its U
 // and AU fragments from HBM kLrAhead k-steps ahead.  Persistent over tiles.
-template <int C, int NT>
+// XO (two-term walk start): only x = U y + beta^2 * cnt; the residual comes
+// from one K1 SpMM on x instead of the (AU) y product.
+template <int C, int NT, bool XO = false>
 __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
     lowrank_init_kernel(kz_eigen h, const double* __restrict__ y, double* __restrict__ x, double* __restrict__ r,
                         double* __restrict__ p, int64_t ldv, int j0, int jmax,
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
             for (int m = 0; m < kLrMT; ++m) {
                 const bool ok = s < nsteps;
                 fu[s][m] = ok ? __ldcs(up[m] + 4 * s) : 0.0;
-                fw[s][m] = ok ? __ldcs(wp[m] + 4 * s) : 0.0;
+                fw[s][m] = ok && !XO ? __ldcs(wp[m] + 4 * s) : 0.0;
             }
         for (int s0 = 0; s0 < nsteps; s0 += kLrAhead) {
 #pragma unroll
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
                     cw[m] = fw[u][m];
                     const bool ok = s + kLrAhead < nsteps;
                     fu[u][m] = ok ? __ldcs(up[m] + 4 * (s + kLrAhead)) : 0.0;
-                    fw[u][m] = ok ? __ldcs(wp[m] + 4 * (s + kLrAhead)) : 0.0;
+                    if constexpr (!XO) fw[u][m] = ok ? __ldcs(wp[m] + 4 * (s + kLrAhead)) : 0.0;
                 }
                 if (s < nsteps) {
                     double bv[NT];
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
 #pragma unroll
                         for (int n = 0; n < NT; ++n) {
                             lr_dmma(ua[m][n][0], ua[m][n][1], cu[m], bv[n]);
-                            lr_dmma(wa[m][n][0], wa[m][n][1], cw[m], bv[n]);
+                            if constexpr (!XO) lr_dmma(wa[m][n][0], wa[m][n][1], cw[m], bv[n]);
                         }
                 }
             }
@@ -165,6 +169,15 @@ __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
                     const int j = j0 + n * 8 + 2 * fk + e;
                     if (j >= jmax) continue;
                     const size_t off = static_cast<size_t>(j / C) * ldv + static_cast<size_t>(row) * C + (j % C);
+                    if constexpr (XO) {
+                        double x0 = ua[m][n][e];
+                        if (cnt) {
+                            const int32_t c = __ldcs(cnt + off);
+                            if (c) x0 = __dadd_rn(x0, __dmul_rn(__dmul_rn(h.beta, h.beta), static_cast<double>(c)));
+                        }
+                        x[off] = x0;
+                        continue;
+                    }
                     const double x0 = ua[m][n][e];
                     x[off] = x0;
                     double r0 = __dsub_rn(__dmul_rn(h.beta, wa[m][n][e]), x0);

@@ -19,7 +19,8 @@ solve order, same ids) and adds, in that order:
 * AU = A U: one K1 SpMM of the r-column block;
 * T = U'AU and W = (I - beta T)^-1 (r x r).
 
-* A2U = A (AU) (walk start, ``walk_terms=1``, the default): one more K1 SpMM.
+* A2U = A (AU) (walk start, ``walk_terms=1``) or A3U = A (A (AU))
+  (two-term walk start, ``walk_terms=2``, the default): one or two more K1 SpMMs.
 
 A query's low-rank term is the Galerkin point of span(U),
 x0 = U W U' b with U' b = beta (AU)[q, :]' -- exact for any orthonormal U, so
@@ -36,6 +37,12 @@ r0 = beta^2 A^2 e_q - U y + beta (AU) y, where A^2 e_q is the integer count
 of 2-walks from q (a sparse push over the neighbours' lists, order-free
 integer atomics).  Measured effect: the CG correction needs one iteration
 fewer (R-MAT 16 prototype: 5 -> 4 at r = 128, 5.5 -> 4.5 at r = 32).
+
+Two-term walk start (``walk_terms=2``): x0 = beta A e_q + beta^2 A^2 e_q + U y
+with y = beta^3 W (A^3 U)[q, :]' (the Galerkin step on the remainder
+beta^3 A^3 e_q); the 2-walk counts give the second term, and r0 = b - M x0
+comes from one K1 SpMM on x0 -- which replaces the (AU) y GEMM of the start --
+so one more CG iteration disappears for the price of that SpMM.
 """
 
 from __future__ import annotations
@@ -54,7 +61,7 @@ class EigenIndex:
 
     solver_kind = "eigen"
 
-    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM", walk_terms=1):
+    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM", walk_terms=2):
         from .build import lanczos_topk
 
         if not isinstance(gi, GraphIndex):
@@ -69,8 +76,8 @@ class EigenIndex:
         rank = int(rank)
         if not 1 <= rank <= min(n, 384):
             raise ValueError(f"rank {rank} outside [1, min(n, 384)]")
-        if walk_terms not in (0, 1):
-            raise ValueError("walk_terms must be 0 (Galerkin start) or 1 (first Katz term exact)")
+        if walk_terms not in (0, 1, 2):
+            raise ValueError("walk_terms must be 0 (Galerkin start), 1 or 2 (Katz terms put in exactly)")
         self.walk_terms = int(walk_terms)
         t0 = time.perf_counter()
         op = gi.operator()
@@ -90,10 +97,14 @@ class EigenIndex:
         ut[:r] = torch.as_tensor(np.ascontiguousarray(lr.vectors.T), device="cuda")
         aut = torch.zeros_like(ut)
         op.spmm(ut[:r].contiguous(), aut[:r], b=r, chunk=1)
-        a2ut = None
+        a2ut = a3ut = None
         if self.walk_terms:
             a2ut = torch.zeros_like(ut)
             op.spmm(aut[:r].contiguous(), a2ut[:r], b=r, chunk=1)
+        if self.walk_terms == 2:
+            a3ut = torch.zeros_like(ut)
+            op.spmm(a2ut[:r].contiguous(), a3ut[:r], b=r, chunk=1)
+            a2ut = None  # the two-term start needs A^3 U only
         t = ut[:r] @ aut[:r].T
         t = 0.5 * (t + t.T)
         w = torch.linalg.inv(torch.eye(r, dtype=torch.float64, device="cuda") - self.alpha * t)
@@ -101,15 +112,17 @@ class EigenIndex:
         self.au = aut.T.contiguous()    # n x ldr row-major
         self.w = w.contiguous()
         self.a2u = a2ut.T.contiguous() if a2ut is not None else None  # n x ldr row-major
+        self.a3u = a3ut.T.contiguous() if a3ut is not None else None
         self.ritz_values = lr.values.copy()
         self.rank, self.ldr = r, ldr
-        del ut, aut, a2ut
+        del ut, aut, a2ut, a3ut
         desc = _lib.KzEigenDesc()
         desc.n, desc.r, desc.ldr = n, r, ldr
         desc.beta = float(self.alpha)
         desc.op = op.handle.value
         desc.u, desc.au, desc.w = self.u.data_ptr(), self.au.data_ptr(), self.w.data_ptr()
         desc.a2u = self.a2u.data_ptr() if self.a2u is not None else None
+        desc.a3u = self.a3u.data_ptr() if self.a3u is not None else None
         h = ctypes.c_void_p()
         _lib.check(lib.kz_eigen_create(ctypes.byref(desc), ctypes.byref(h)))
         self._lib, self._handle = lib, h
@@ -141,14 +154,21 @@ class EigenIndex:
             u, au = u[inv], au[inv]
         return u, au, self.w.cpu().numpy()
 
+    def _internal_rows(self, t):
+        if t is None:
+            return None
+        m = t[:, : self.rank].cpu().numpy()
+        inv = getattr(self.gi, "_inv", None) if getattr(self.gi, "_order", None) is not None else None
+        return m[inv] if inv is not None else m
+
     def a2u_internal(self):
         """A^2 U as a host array with rows in internal node order (None
-        without the walk start)."""
-        if self.a2u is None:
-            return None
-        a2u = self.a2u[:, : self.rank].cpu().numpy()
-        inv = getattr(self.gi, "_inv", None) if getattr(self.gi, "_order", None) is not None else None
-        return a2u[inv] if inv is not None else a2u
+        unless walk_terms == 1)."""
+        return self._internal_rows(self.a2u)
+
+    def a3u_internal(self):
+        """A^3 U, internal row order (None unless walk_terms == 2)."""
+        return self._internal_rows(self.a3u)
 
     # -- the GraphIndex surface (ids, operator, masks) ----------------------
     @property
