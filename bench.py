@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solver", default="eigen", choices=["eigen", "cg"])
-    ap.add_argument("--walk-terms", type=int, default=2, choices=[0, 1, 2],
+    ap.add_argument("--walk-terms", type=int, default=3, choices=[0, 1, 2, 3],
                     help="eigen start: Katz-series terms put in exactly before the Galerkin step (0, 1, 2)")
     return ap.parse_args()
 
@@ -330,7 +330,8 @@ def main():
                        "solver": (f"LRC-Katz, eigen form: rank-{eidx.rank} eigen index of A (low-rank Galerkin "
                                   f"term, two fp64 DMMA GEMMs"
                                   + ({0: "", 1: ", first Katz term beta*A*e_q exact via 2-walk counts",
-                                      2: ", first two Katz terms exact (2-walk counts), r0 from one SpMM"}[eidx.walk_terms])
+                                      2: ", first two Katz terms exact (2-walk counts), r0 from one SpMM",
+                                      3: ", first three Katz terms exact (2-walk counts + one SpMM), r0 from one SpMM"}[eidx.walk_terms])
                                   + ") + CG correction" if eidx is not None
                                   else "plain CG (query_cg_baseline)"),
                        "eigen_index_build_s": round(t_index, 2) if eidx is not None else None,

@@ -231,7 +231,9 @@ int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const in
  * counts from q (an integer sparse push, no SpMM): one CG iteration fewer.
  * With a3u = A^3 U the start carries the first two terms, x0 = beta A e_q +
  * beta^2 A^2 e_q + U y, y = beta^3 W (A^3 U)[q,:]', and r0 comes from one
- * SpMM on x0 (no (AU) y product): one more CG iteration fewer. */
+ * SpMM on x0 (no (AU) y product): one more CG iteration fewer.  With a4u =
+ * A^4 U the third term beta^3 A^3 e_q is added by one more SpMM on the
+ * beta^2 A^2 e_q block and y = beta^4 W (A^4 U)[q,:]': one more again. */
 typedef struct kz_eigen kz_eigen;
 typedef struct kz_eigen_desc {
     int64_t n, r;
@@ -243,6 +245,8 @@ typedef struct kz_eigen_desc {
     const double* w;      /* device r x r row-major, (I - beta U'AU)^-1 */
     const double* a2u;    /* device n x ldr row-major, A^2 U; NULL: plain Galerkin start */
     const double* a3u;    /* device n x ldr row-major, A^3 U: two-term walk start (takes precedence) */
+    const double* a4u;    /* device n x ldr row-major, A^4 U: three-term walk start (x0 += beta^3 A^3 e_q
+                             by one more SpMM on the 2-walk counts; takes precedence) */
 } kz_eigen_desc;
 int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out);
 int kz_eigen_destroy(kz_eigen* h);

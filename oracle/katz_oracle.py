@@ -118,14 +118,20 @@ def query_cg_csr(a, beta, q, tol=1e-8, max_iter=None, start_seed=None):
 # ---------------------------------------------------------------------------
 
 
-def query_eigen_csr(a, beta, q, u, au, w, tol=1e-8, max_iter=None, a2u=None, a3u=None):
+def query_eigen_csr(a, beta, q, u, au, w, tol=1e-8, max_iter=None, a2u=None, a3u=None, a4u=None):
     """Scores (clamped) and report of one query, eigen-form start + cg.
     With a2u (= A^2 U) the walk start: x0 = beta A e_q + U y with
     y = beta^2 W (A^2 U)[q]' (the Galerkin step on the remainder)."""
     n = a.shape[0]
     rhs = np.zeros(n)
     rhs[a.indices[a.indptr[q] : a.indptr[q + 1]]] = beta
-    if a3u is not None:
+    if a4u is not None:
+        # three-term walk start: x0 = beta A e_q + beta^2 A^2 e_q + beta^3 A^3 e_q + U y,
+        # y = beta^4 W (A^4 U)[q]'
+        y = (beta ** 4) * (w @ a4u[q])
+        a2e = a @ (a @ np.eye(1, n, q).ravel())
+        x0 = rhs + (beta * beta) * a2e + (beta ** 3) * (a @ a2e) + u @ y
+    elif a3u is not None:
         # two-term walk start: x0 = beta A e_q + beta^2 A^2 e_q + U y,
         # y = beta^3 W (A^3 U)[q]'
         y = (beta * beta * beta) * (w @ a3u[q])

@@ -133,6 +133,7 @@ class KzEigenDesc(ctypes.Structure):
         ("w", ctypes.c_void_p),
         ("a2u", ctypes.c_void_p),
         ("a3u", ctypes.c_void_p),
+        ("a4u", ctypes.c_void_p),
     ]
 
 

@@ -217,7 +217,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         const size_t smem = lowrank_smem(eig->ldr, 8 * nt);
         // walk start: 2-walk counts into the (still unused) q block, int32
         int32_t* cnt = nullptr;
-        const bool two_term = eig->a3u != nullptr;
+        const bool three_term = eig->a4u != nullptr;
+        const bool two_term = eig->a3u != nullptr || three_term;
         if (eig->a2u || two_term) {
             cnt = reinterpret_cast<int32_t*>(w.q);
             KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
@@ -238,7 +239,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                 KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN, true>,                                \
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
                 lowrank_init_kernel<CC, NN, true><<<lgrid, 32 * kLrWarps, smem, st>>>(*eig, w.y, w.x, nullptr, \
-                                                                                      nullptr, n * CC, j0, w.bpad, cnt); \
+                                                                                      nullptr, n * CC, j0, w.bpad, cnt, \
+                                                                                      three_term ? w.p : nullptr); \
             } else {                                                                                           \
                 KZ_CUDA(cudaFuncSetAttribute(lowrank_init_kernel<CC, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                              static_cast<int>(smem)));                                         \
@@ -261,6 +263,21 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                                                                                 w.qpos, b, a->beta, s.bnorm2);
                       ::kz::note_launch());
         KZ_LAUNCH_CHECK();
+        if (three_term) {
+            // third Katz term: x0 += beta * A (beta^2 A^2 e_q), one K1 SpMM on
+            // the count block the low-rank kernel left in p
+            SpmmArgs sa = make_spmm_args(g, w.sp);
+            sa.Xg = w.p;
+            sa.Xs = nullptr;
+            sa.Z = w.x;
+            sa.Y = w.x;
+            sa.s0 = 1.0;
+            sa.s1 = 0.0;
+            sa.s2 = a->beta;
+            sa.want_dot = 0;
+            sa.chunk_active = nullptr;
+            if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
+        }
         if (two_term) {
             // r0 = b - (x0 - beta A x0): one K1 SpMM on x0 (exactly consistent
             // with x0), then the rhs scattered on top
@@ -462,6 +479,7 @@ extern "C" int kz_eigen_create(const kz_eigen_desc* d, kz_eigen** out) {
     h->w = d->w;
     h->a2u = d->a2u;
     h->a3u = d->a3u;
+    h->a4u = d->a4u;
     *out = h;
     return KZ_OK;
 }

@@ -36,6 +36,7 @@ struct kz_eigen {
     const double* w = nullptr;      // device r x r row-major, symmetric
     const double* a2u = nullptr;    // optional device n x ldr row-major, A^2 U (walk start)
     const double* a3u = nullptr;    // optional device n x ldr row-major, A^3 U (two-term walk start)
+    const double* a4u = nullptr;    // optional device n x ldr row-major, A^4 U (three-term walk start)
 };
 
 namespace kz {
@@ -50,11 +51,12 @@ __global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos
     if (k >= h.ldr) return;
     double s = 0.0;
     if (j < b && k < h.r) {
-        const double* __restrict__ aurow = (h.a3u ? h.a3u : h.a2u ? h.a2u : h.au) + qpos[j] * h.ldr;
+        const double* __restrict__ aurow =
+            (h.a4u ? h.a4u : h.a3u ? h.a3u : h.a2u ? h.a2u : h.au) + qpos[j] * h.ldr;
         const double* __restrict__ wrow = h.w + k * h.r;
         for (int64_t i = 0; i < h.r; ++i) s = fma(wrow[i], __ldg(aurow + i), s);
         const double b2 = __dmul_rn(h.beta, h.beta);
-        s *= h.a3u ? __dmul_rn(b2, h.beta) : h.a2u ? b2 : h.beta;
+        s *= h.a4u ? __dmul_rn(b2, b2) : h.a3u ? __dmul_rn(b2, h.beta) : h.a2u ? b2 : h.beta;
     }
     y[static_cast<size_t>(j / C) * h.ldr * C + static_cast<size_t>(k) * C + (j % C)] = s;
 }
@@ -91,7 +93,7 @@ template <int C, int NT, bool XO = false>
 __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
     lowrank_init_kernel(kz_eigen h, const double* __restrict__ y, double* __restrict__ x, double* __restrict__ r,
                         double* __restrict__ p, int64_t ldv, int j0, int jmax,
-                        const int32_t* __restrict__ cnt = nullptr) {
+                        const int32_t* __restrict__ cnt = nullptr, double* __restrict__ cnt_out = nullptr) {
     constexpr int NC = 8 * NT;
     constexpr int YLD = NC + 8;
     extern __shared__ __align__(16) double ys[];
@@ -171,11 +173,16 @@ __global__ void __launch_bounds__(32 * kLrWarps, KZ_LR_MINBLOCKS)
                     const size_t off = static_cast<size_t>(j / C) * ldv + static_cast<size_t>(row) * C + (j % C);
                     if constexpr (XO) {
                         double x0 = ua[m][n][e];
+                        double t2 = 0.0;  // beta^2 (A^2 e_q)_row
                         if (cnt) {
                             const int32_t c = __ldcs(cnt + off);
-                            if (c) x0 = __dadd_rn(x0, __dmul_rn(__dmul_rn(h.beta, h.beta), static_cast<double>(c)));
+                            if (c) {
+                                t2 = __dmul_rn(__dmul_rn(h.beta, h.beta), static_cast<double>(c));
+                                x0 = __dadd_rn(x0, t2);
+                            }
                         }
                         x[off] = x0;
+                        if (cnt_out) cnt_out[off] = t2;  // three-term start: input of the A^3 e_q SpMM
                         continue;
                     }
                     const double x0 = ua[m][n][e];

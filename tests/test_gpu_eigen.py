@@ -40,7 +40,7 @@ def exact(a, alpha, internal):
     return np.asarray(spsolve(m, rhs)).reshape(a.shape[0], -1).T
 
 
-@pytest.mark.parametrize("walk", [0, 1, 2])
+@pytest.mark.parametrize("walk", [0, 1, 2, 3])
 @pytest.mark.parametrize("beta", [0.5, 0.95])
 @pytest.mark.parametrize("rank,b", [(1, 1), (8, 5), (30, 37), (64, 64)])
 @pytest.mark.parametrize("tol", [1e-8, 1e-12])
@@ -126,7 +126,7 @@ def test_eigen_tiny_graphs_full_rank(env, edges, rank):
         assert reps[j].converged
 
 
-@pytest.mark.parametrize("walk", [0, 1, 2])
+@pytest.mark.parametrize("walk", [0, 1, 2, 3])
 @pytest.mark.parametrize("reorder", [None, "rcm"])
 def test_eigen_matches_cpu_oracle_of_the_same_algorithm(env, reorder, walk):
     """GPU eigen-form LRC against its CPU restatement (oracle.query_eigen_csr:
@@ -142,13 +142,14 @@ def test_eigen_matches_cpu_oracle_of_the_same_algorithm(env, reorder, walk):
     u, au, w = ei.basis_internal()
     a2u = ei.a2u_internal()
     a3u = ei.a3u_internal()
-    assert (a2u is None) == (walk != 1) and (a3u is None) == (walk != 2)
+    a4u = ei.a4u_internal()
+    assert (a2u is None) == (walk != 1) and (a3u is None) == (walk != 2) and (a4u is None) == (walk != 3)
     qs = g.original_ids[np.linspace(0, g.n - 1, 12).astype(int)]
     for tol in (1e-8, 1e-10):
         scores, reps = kz.query_batch(ei, qs, tol=tol)
         for j, q in enumerate(qs):
             want, orep = O.query_eigen_csr(a.tocsr(), alpha, int(np.searchsorted(g.original_ids, q)), u, au, w,
-                                           tol=tol, a2u=a2u, a3u=a3u)
+                                           tol=tol, a2u=a2u, a3u=a3u, a4u=a4u)
             assert abs(reps[j].iterations - orep.iterations) <= 1, (j, reps[j].iterations, orep.iterations)
             assert np.linalg.norm(scores[j] - want) <= 1e-10 * np.linalg.norm(want)
 
@@ -185,3 +186,10 @@ def test_walk_start_saves_iterations_and_is_deterministic(env):
     assert np.all(diff <= 2 * cond * 1e-8), diff.max()
     s2b, _ = kz.query_batch(e2, qs, tol=1e-8, device=True)
     assert torch.equal(s2, s2b)
+    # three-term: never more iterations than two-term
+    e3 = kz.EigenIndex(gi, 32, walk_terms=3)
+    s3, r3 = kz.query_batch(e3, qs, tol=1e-8, device=True)
+    it3 = np.array([r.iterations for r in r3])
+    assert np.all(it3 <= it2), (it2.mean(), it3.mean())
+    diff = (torch.linalg.vector_norm(s3 - s0, dim=1) / torch.linalg.vector_norm(s0, dim=1)).cpu().numpy()
+    assert np.all(diff <= 2 * cond * 1e-8), diff.max()

@@ -113,11 +113,11 @@ def test_rmat_scale_eigen_form(kz, cfg):
     assert torch.equal(s_e, s_e2)
     # sampled columns against the CPU restatement of the same algorithm
     u, au, w = ei.basis_internal()
-    a2u, a3u = ei.a2u_internal(), ei.a3u_internal()
+    a2u, a3u, a4u = ei.a2u_internal(), ei.a3u_internal(), ei.a4u_internal()
     a = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
     for j in (0, len(qs) - 1):
         want, orep = O.query_eigen_csr(a, gi.alpha, g.internal_id(int(qs[j])), u, au, w, tol=spec["tol"], a2u=a2u,
-                                       a3u=a3u)
+                                       a3u=a3u, a4u=a4u)
         got = s_e[j].cpu().numpy()
         assert abs(r_e[j].iterations - orep.iterations) <= 1
         assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-10
