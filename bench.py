@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solver", default="eigen", choices=["eigen", "cg"])
-    ap.add_argument("--walk-terms", type=int, default=3, choices=[0, 1, 2, 3],
+    ap.add_argument("--walk-terms", type=int, default=None, choices=[0, 1, 2, 3],
                     help="eigen start: Katz-series terms put in exactly before the Galerkin step (0, 1, 2)")
     return ap.parse_args()
 

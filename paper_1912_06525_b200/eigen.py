@@ -44,7 +44,8 @@ beta^3 A^3 e_q); the 2-walk counts give the second term, and r0 = b - M x0
 comes from one K1 SpMM on x0 -- which replaces the (AU) y GEMM of the start --
 so one more CG iteration disappears for the price of that SpMM.
 
-Three-term walk start (``walk_terms=3``, the default): x0 also carries
+Three-term walk start (``walk_terms=3``, the default above 10^6 stored
+entries; one term below): x0 also carries
 beta^3 A^3 e_q, one K1 SpMM on the beta^2 A^2 e_q block, and y uses A^4 U;
 R-MAT 22: 2 CG iterations instead of 3 (1.97 mean).
 """
@@ -65,7 +66,7 @@ class EigenIndex:
 
     solver_kind = "eigen"
 
-    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM", walk_terms=3):
+    def __init__(self, gi, rank, lanczos_tol=1e-8, seed=0, max_steps=None, which="LM", walk_terms=None):
         from .build import lanczos_topk
 
         if not isinstance(gi, GraphIndex):
@@ -80,6 +81,12 @@ class EigenIndex:
         rank = int(rank)
         if not 1 <= rank <= min(n, 384):
             raise ValueError(f"rank {rank} outside [1, min(n, 384)]")
+        if walk_terms is None:
+            # each extra term costs one SpMM in the start and removes one CG
+            # iteration (SpMM + vector passes): a win once SpMMs dominate the
+            # launch overheads -- measured: cfg1 (10^5 entries) is fastest with
+            # one term, R-MAT 16-22 (10^6-10^8) with three
+            walk_terms = 3 if gi.graph.nnz > 1_000_000 else 1
         if walk_terms not in (0, 1, 2, 3):
             raise ValueError("walk_terms must be 0 (Galerkin start), 1, 2 or 3 (Katz terms put in exactly)")
         self.walk_terms = int(walk_terms)
