@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solver", default="eigen", choices=["eigen", "cg"])
+    ap.add_argument("--reorder", default="auto", help="GraphIndex solve order (auto | degclass | rcm | none)")
     ap.add_argument("--walk-terms", type=int, default=None, choices=[0, 1, 2, 3],
                     help="eigen start: Katz-series terms put in exactly before the Galerkin step (0, 1, 2)")
     return ap.parse_args()
@@ -182,7 +183,7 @@ def main():
     t_graph = time.perf_counter() - t0
     lam = kz.spectral_norm(g)
     beta = 0.5 / lam
-    idx = kz.GraphIndex(g, beta, spectral_norm=lam)
+    idx = kz.GraphIndex(g, beta, spectral_norm=lam, reorder=args.reorder)
     op = idx.operator()
     qs = G.sample_queries(g.original_ids, b, seed=rank)
     internal = idx.internal_ids(qs)

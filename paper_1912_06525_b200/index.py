@@ -271,8 +271,8 @@ class GraphIndex(_DeviceGraphMixin):
     with rhs alpha*A e_q, i.e. query_cg_baseline in natural order.
 
     ``reorder`` relabels the nodes *inside the solve* for gather locality
-    (reverse Cuthill-McKee; "auto" = only for operators above 10^6 stored
-    entries).  It is invisible at the API: right-hand sides, start vectors
+    ("degclass": degree classes, reverse Cuthill-McKee inside each; "rcm";
+    "degree"; "auto" = "degclass" for operators above 10^6 stored entries).  It is invisible at the API: right-hand sides, start vectors
     and scores stay in internal order (the output kernel scatters back); only
     summation order, i.e. roundoff, changes.
     """
@@ -289,10 +289,12 @@ class GraphIndex(_DeviceGraphMixin):
         g = self.graph
         mode = self.reorder
         if mode == "auto":
-            mode = "rcm" if g.nnz > 1_000_000 else None
+            mode = "degclass" if g.nnz > 1_000_000 else None
         self._order = None
         if mode == "rcm":
             self._order = rcm_order(g)
+        elif mode == "degclass":
+            self._order = degclass_rcm_order(g)
         elif mode == "degree":
             self._order = np.argsort(-np.diff(g.row_offsets), kind="stable")
         elif mode not in (None, "none"):
@@ -362,6 +364,19 @@ def rcm_order(g):
 
     a = sp.csr_matrix((np.ones(g.nnz, dtype=np.int8), g.col_indices, g.row_offsets), shape=(g.n, g.n))
     return np.asarray(csgraph.reverse_cuthill_mckee(a, symmetric_mode=True), dtype=np.int64)
+
+
+def degclass_rcm_order(g):
+    """Rows grouped by degree class (floor(log2 deg), highest first), RCM
+    order inside each class: rows of similar degree -- which in a power-law
+    graph share their hub neighbours -- run together, so K1's gathered rows
+    stay in L2 longer (R-MAT 22: K1 18.1 -> 17.4 ms against plain RCM,
+    tools/reorder_minhash.py)."""
+    rcm = rcm_order(g)
+    pos = np.empty(g.n, dtype=np.int64)
+    pos[rcm] = np.arange(g.n)
+    cls = -np.floor(np.log2(np.maximum(np.diff(g.row_offsets), 1))).astype(np.int64)
+    return np.lexsort((pos, cls)).astype(np.int64)
 
 
 def permute_csr(offsets, cols, order, inv):

@@ -1,0 +1,85 @@
+"""K1 (C = 32, b = 256) at R-MAT 22 under row orders that group rows with
+similar neighbourhoods (min-hash signatures), against RCM: rows processed
+together then share more gathered rows in L2.
+
+    python tools/reorder_minhash.py [scale]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+from paper_1912_06525_b200 import generators as G
+from paper_1912_06525_b200.index import rcm_order
+
+import time  # noqa: E402
+
+import torch  # noqa: E402
+
+import paper_1912_06525_b200 as kz  # noqa: E402
+from paper_1912_06525_b200.index import permute_csr  # noqa: E402
+
+
+def timeit(g, order, b=256, C=32):
+    """min of 3 timed K1 launches (after one warm-up) in this order"""
+    inv = np.empty(g.n, dtype=np.int64)
+    inv[order] = np.arange(g.n)
+    off, c = permute_csr(g.row_offsets, g.col_indices, order, inv)
+    op = kz.DeviceOperator(off, c, g.n)
+    X = torch.randn(b * g.n, dtype=torch.float64, device="cuda")
+    Y = torch.empty_like(X)
+    dots = torch.empty(b, dtype=torch.float64, device="cuda")
+    ts = []
+    for _ in range(4):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        op.spmm(X, Y, b=b, chunk=C, Xs=X, s1=1.0, s2=-1e-4, dots=dots)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t)
+    del X, Y, op
+    torch.cuda.empty_cache()
+    return round(min(ts[1:]) * 1e3, 2)
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
+g = G.rmat_graph_fast(scale)
+n = g.n
+rp = g.row_offsets.astype(np.int64)
+col = g.col_indices.astype(np.int64)
+deg = np.diff(rp)
+rcm = rcm_order(g)
+print("rcm", timeit(g, rcm), flush=True)
+rng = np.random.default_rng(0)
+sig = []
+for k in range(2):
+    h = rng.permutation(n).astype(np.int64)
+    hv = h[col]
+    m = np.minimum.reduceat(hv, rp[:-1]) if g.nnz else np.zeros(n, np.int64)
+    m[deg == 0] = n
+    sig.append(m)
+o1 = np.lexsort((np.arange(n), sig[0]))
+print("minhash1", timeit(g, o1), flush=True)
+o2 = np.lexsort((sig[1], sig[0]))
+print("minhash2", timeit(g, o2), flush=True)
+# RCM blocks of 4096 rows, min-hash sorted inside each block
+pos = np.empty(n, np.int64)
+pos[rcm] = np.arange(n)
+o3 = np.lexsort((sig[0][rcm], pos[rcm] // 4096))
+print("rcm_blocks_minhash", timeit(g, rcm[o3]), flush=True)
+# degree-descending, min-hash inside equal-degree-class (log2 bins)
+cls = -np.floor(np.log2(np.maximum(deg, 1))).astype(np.int64)
+o4 = np.lexsort((sig[0], cls))
+print("degclass_minhash", timeit(g, o4), flush=True)
+
+# variants of the degree-class order
+pos = np.empty(n, np.int64)
+pos[rcm] = np.arange(n)
+o5 = np.lexsort((pos, cls))
+print("degclass_rcm", timeit(g, o5), flush=True)
+cls4 = -np.floor(np.log2(np.maximum(deg, 1)) / 2).astype(np.int64)
+o6 = np.lexsort((sig[0], cls4))
+print("degclass4_minhash", timeit(g, o6), flush=True)
+o7 = np.lexsort((sig[1], sig[0], cls))
+print("degclass_minhash2", timeit(g, o7), flush=True)
+print("rcm", timeit(g, rcm), flush=True)
+print("degclass_minhash", timeit(g, o4), flush=True)
