@@ -71,15 +71,15 @@ cls = -np.floor(np.log2(np.maximum(deg, 1))).astype(np.int64)
 o4 = np.lexsort((sig[0], cls))
 print("degclass_minhash", timeit(g, o4), flush=True)
 
-# variants of the degree-class order
+# variants of the degree-class order (RCM inside each class)
 pos = np.empty(n, np.int64)
 pos[rcm] = np.arange(n)
-o5 = np.lexsort((pos, cls))
-print("degclass_rcm", timeit(g, o5), flush=True)
-cls4 = -np.floor(np.log2(np.maximum(deg, 1)) / 2).astype(np.int64)
-o6 = np.lexsort((sig[0], cls4))
-print("degclass4_minhash", timeit(g, o6), flush=True)
-o7 = np.lexsort((sig[1], sig[0], cls))
-print("degclass_minhash2", timeit(g, o7), flush=True)
-print("rcm", timeit(g, rcm), flush=True)
-print("degclass_minhash", timeit(g, o4), flush=True)
+lg = np.log2(np.maximum(deg, 1))
+for name, key in (("degclass_rcm", -np.floor(lg)),
+                  ("halfoctave_rcm", -np.floor(2 * lg)),
+                  ("ascending_rcm", np.floor(lg)),
+                  ("two_classes_1024_rcm", -(deg > 1024).astype(np.int64)),
+                  ("three_classes_rcm", -((deg > 32).astype(np.int64) + (deg > 1024).astype(np.int64))),
+                  ("degclass_rcm", -np.floor(lg))):
+    o = np.lexsort((pos, key.astype(np.int64)))
+    print(name, timeit(g, o), flush=True)
