@@ -71,15 +71,26 @@ cls = -np.floor(np.log2(np.maximum(deg, 1))).astype(np.int64)
 o4 = np.lexsort((sig[0], cls))
 print("degclass_minhash", timeit(g, o4), flush=True)
 
-# variants of the degree-class order (RCM inside each class)
+# degree classes, each ordered by the RCM of its own induced subgraph
+import scipy.sparse as sp  # noqa: E402
+import scipy.sparse.csgraph as csgraph  # noqa: E402
+
 pos = np.empty(n, np.int64)
 pos[rcm] = np.arange(n)
 lg = np.log2(np.maximum(deg, 1))
-for name, key in (("degclass_rcm", -np.floor(lg)),
-                  ("halfoctave_rcm", -np.floor(2 * lg)),
-                  ("ascending_rcm", np.floor(lg)),
-                  ("two_classes_1024_rcm", -(deg > 1024).astype(np.int64)),
-                  ("three_classes_rcm", -((deg > 32).astype(np.int64) + (deg > 1024).astype(np.int64))),
-                  ("degclass_rcm", -np.floor(lg))):
-    o = np.lexsort((pos, key.astype(np.int64)))
-    print(name, timeit(g, o), flush=True)
+cls = -np.floor(lg).astype(np.int64)
+print("degclass_rcm", timeit(g, np.lexsort((pos, cls))), flush=True)
+A = sp.csr_matrix((np.ones(g.nnz, dtype=np.int8), g.col_indices, g.row_offsets), shape=(n, n))
+parts = []
+for c in np.unique(cls):
+    nodes = np.nonzero(cls == c)[0]
+    sub = A[nodes][:, nodes]
+    o = np.asarray(csgraph.reverse_cuthill_mckee(sub.tocsr(), symmetric_mode=True), dtype=np.int64)
+    parts.append(nodes[o])
+print("degclass_subrcm", timeit(g, np.concatenate(parts)), flush=True)
+# classes by the degree of the row's largest neighbour (its hub), RCM inside
+hubdeg = np.maximum.reduceat(deg[col], rp[:-1])
+hcls = -np.floor(np.log2(np.maximum(hubdeg, 1))).astype(np.int64)
+print("hubclass_rcm", timeit(g, np.lexsort((pos, hcls))), flush=True)
+print("degclass_then_hubclass_rcm", timeit(g, np.lexsort((pos, hcls, cls))), flush=True)
+print("degclass_rcm", timeit(g, np.lexsort((pos, cls))), flush=True)
