@@ -405,8 +405,18 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
     const int gw = lane / K::G, lg = lane % K::G, gbase = gw * K::G;
     const unsigned gmask = (K::G == 32) ? 0xffffffffu : (((1u << K::G) - 1u) << gbase);
     const int total = a.ngroups * a.nchunks;
+    // the solve loop issues one iteration ahead of its stop poll: when every
+    // column has already stopped, leave at once instead of draining the
+    // queue through masked chunks (the queue and counters stay armed; a
+    // warp that skips still counts itself out below, so the last warp
+    // re-arms the queue either way)
+    int idle_l = 0;  // read by one lane: the loop below is warp-synchronous
+    if (lane == 0)
+        idle_l = a.hook.mode == 1 && a.hook.n_active &&
+                 *reinterpret_cast<volatile const int32_t*>(a.hook.n_active) == 0;
+    const bool idle = __shfl_sync(0xffffffffu, idle_l, 0) != 0;
 
-    while (true) {
+    while (!idle) {
         int g = 0;
         if (lane == 0) g = atomicAdd(a.queue, 1);
         g = __shfl_sync(0xffffffffu, g, 0);
