@@ -62,7 +62,10 @@ __global__ void lowrank_coef_kernel(kz_eigen h, const int64_t* __restrict__ qpos
 }
 
 constexpr int kLrWarps = 8;
-constexpr int kLrMT = 1;                           // m-fragments (8 rows) per warp (2 spills)
+#ifndef KZ_LR_MT
+#define KZ_LR_MT 1
+#endif
+constexpr int kLrMT = KZ_LR_MT;                    // m-fragments (8 rows) per warp (2 spills)
 constexpr int kLrRows = 8 * kLrMT * kLrWarps;      // rows per tile
 #ifndef KZ_LR_AHEAD
 #define KZ_LR_AHEAD 4
