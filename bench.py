@@ -92,7 +92,30 @@ class ClockSampler:
             if len(parts) == 6:
                 self.rows.append(parts)
 
-    def stop(self):
+    def wait_ready(self, timeout=5.0):
+        """Block until nvidia-smi has printed its first row (its start-up
+        takes longer than a short timed region)."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        return len(self.rows)
+
+    def extend_under_load(self, step, min_samples, timeout=5.0):
+        """When the timed region was shorter than the sampling interval, keep
+        running untimed steps of the same workload until `min_samples` rows
+        have arrived since the timed region began (bounded by `timeout`)."""
+        import torch
+
+        if self.proc is None:
+            return 0
+        base, t0, extra = len(self.rows), time.perf_counter(), 0
+        while len(self.rows) - base < min_samples and time.perf_counter() - t0 < timeout:
+            step()
+            torch.cuda.synchronize()
+            extra += 1
+        return extra
+
+    def stop(self, first=0, extra_steps=0):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -102,7 +125,7 @@ class ClockSampler:
             self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm, smax, reasons = [], [], set()
-        for r in self.rows:
+        for r in self.rows[first:]:
             try:
                 sm.append(float(r[0]))
                 smax.append(float(r[1]))
@@ -113,7 +136,8 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                **({"untimed_steps_sampled": extra_steps} if extra_steps else {})}
 
 
 def build_graph(cfg):
@@ -205,13 +229,15 @@ def main():
         ids, vals, counts = kz.topk_device(scores, k, idx.mask_operator(), internal, internal)
         return reps, ids
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         reps, _ = step()
     torch.cuda.synchronize()
+    clocks.wait_ready()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    first = len(clocks.rows)
     l0 = lib.kz_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -227,7 +253,10 @@ def main():
     launches = lib.kz_launch_count() - l0
     if world > 1:
         dist.barrier()
-    clock_info = clocks.stop()
+    # A short timed region (cfg1/cfg2) ends before the 200 ms sampling
+    # interval: keep the same step running, untimed, until 2 samples exist.
+    extra = clocks.extend_under_load(step, 2 - (len(clocks.rows) - first))
+    clock_info = clocks.stop(first, extra)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
