@@ -58,6 +58,15 @@ const char* kz_last_error(void);
 int kz_version(void);
 /* total kernels this library has launched in the process (bench evidence) */
 long long kz_launch_count(void);
+/* SM count of the current device (every persistent grid is sized from it) */
+int kz_num_sms(void);
+/* K1 launch timing (bench.py's roofline): kz_k1_timing(1) clears and starts
+ * recording a pair of CUDA events around every K1 SpMM launch on its own
+ * stream (launches inside stream capture are not timed); kz_k1_timing_read
+ * synchronises on them and returns the summed launch time and the number
+ * of timed launches.  kz_k1_timing(0) stops recording and frees the events. */
+int kz_k1_timing(int enable);
+int kz_k1_timing_read(double* total_ms, long long* launches);
 
 /* ---- operator handles ------------------------------------------------- */
 
@@ -191,6 +200,13 @@ typedef struct kz_topk_args {
     int64_t* ids_out;
     double* vals_out;
     int32_t* count_out;
+    /* optional exclusive upper bound per column (device double[b] and
+     * int64[b], both or neither): only keys strictly below (bound_vals[j],
+     * bound_ids[j]) in (score desc, id asc) order take part; bound_ids[j] < 0
+     * means no bound.  One call returns at most 4096 entries per column; a
+     * larger k continues from the last key of the previous pass. */
+    const double* bound_vals;
+    const int64_t* bound_ids;
 } kz_topk_args;
 size_t kz_topk_workspace_bytes(int32_t b, int64_t n, int32_t k);
 int kz_topk_batch(const kz_topk_args* a, void* ws, size_t ws_bytes, void* stream);
@@ -201,7 +217,9 @@ int kz_topk_batch(const kz_topk_args* a, void* ws, size_t ws_bytes, void* stream
  * c < counts[j]  (the profile rows of linkpred.py:189-196).
  * kz_pearson_rerank: per query j, corr[c] = Pearson(ref[j], profiles[j][:, c])
  * (0 for zero variance, clipped to [-1, 1]) and the rerank order of
- * lexsort((top, -score, -corr)) (linkpred.py:197-205).  s <= 2048. */
+ * lexsort((top, -score, -corr)) (linkpred.py:197-205), sorted in shared
+ * memory for s <= 8192; order_out == NULL computes the correlations only
+ * (the Python mirror orders s > 8192 candidates with a device sort). */
 int kz_profile_gather(const double* S, int64_t n, int32_t ntrip, const int64_t* trip,
                       const int64_t* top_ids, const int32_t* counts, int32_t s, double* profiles,
                       int32_t T1, void* stream);
@@ -274,8 +292,19 @@ int kz_min_degree_orders(int64_t nparts, const int64_t* bounds, const int64_t* r
                          const int64_t* colidx, int64_t* orders);
 
 /* ---- vector helpers used by the generic cg() / lrc_pcg() drivers -------- */
-/* out[j] = sum_i X[i,j]*Y[i,j] over b columns of length n (column-major). */
-int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out, void* stream);
+/* out[j] = sum_i X[i,j]*Y[i,j] over b columns of length n (column-major);
+ * the numpy `@` dots of solver.py:71-95 / 126-156.  The caller provides the
+ * reduction scratch (kz_coldot_workspace_bytes), so calls on distinct
+ * streams with distinct workspaces are reentrant. */
+size_t kz_coldot_workspace_bytes(int64_t n, int32_t b);
+int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out, void* ws,
+              size_t ws_bytes, void* stream);
+/* Vector update of the generic cg() driver (solver.py:88-99) with the
+ * products and the sum rounded separately, as numpy evaluates them:
+ * op 0: out = a*x + b*y (y == NULL: out = a*x); op 1: out = x / a
+ * (spectral_norm's v = w / ||w||, graph.py:289).  out may alias x or y. */
+int kz_vec_op(int32_t op, int64_t n, double a, const double* x, double b, const double* y, double* out,
+              void* stream);
 
 #ifdef __cplusplus
 }

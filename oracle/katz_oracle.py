@@ -454,3 +454,136 @@ def sparse_katz(solve, neighbors_of, id_map, q_internal, s, T=None):
         corr[ok] = np.clip((ref_c @ pc[:, ok]) / (sr * sp_[ok]), -1.0, 1.0)
     rerank = np.lexsort((top, -scores[top], -corr))
     return [(int(id_map[top[i]]), float(corr[i])) for i in rerank]
+
+
+# ---------------------------------------------------------------------------
+# Input preparation for bench.py --impl reference and the scale tests: the
+# seeded generators of SURVEY.md Appendix B, from_edges (graph.py:111-148),
+# the largest component (graph.py:232-261) and spectral_norm (graph.py:264-297)
+# restated on numpy/scipy only, so the reference arm loads nothing from the
+# product package.  tests/test_oracle_golden.py checks them against the
+# reference's own from_edges / largest_connected_component / spectral_norm
+# outputs (tests/golden/ingest.npz, chunglu2000_cg.npz).
+# ---------------------------------------------------------------------------
+
+RMAT_ABCD = (0.57, 0.19, 0.19, 0.05)
+
+
+def rmat_pairs(scale, edge_factor=16, abcd=RMAT_ABCD, seed=0):
+    """SURVEY Appendix B R-MAT: one uniform per edge and bit, least
+    significant bit first; u_bit = r >= a+b, v_bit = (a <= r < a+b) or
+    r >= a+b+c."""
+    a, b, c, _ = abcd
+    n = 1 << scale
+    m = n * edge_factor
+    rng = np.random.default_rng(seed)
+    u = np.zeros(m, dtype=np.int64)
+    v = np.zeros(m, dtype=np.int64)
+    for bit in range(scale):
+        r = rng.random(m)
+        u |= (r >= a + b).astype(np.int64) << bit
+        v |= (((r >= a) & (r < a + b)) | (r >= a + b + c)).astype(np.int64) << bit
+        del r
+    return u, v, n
+
+
+def chung_lu_pairs(n=10_000, gamma=2.5, mean_degree=10.0, seed=0):
+    """SURVEY Appendix B Chung-Lu: weights i^(-1/(gamma-1)) scaled to the
+    mean degree, n*d/2 pairs drawn i.i.d. proportional to them (u batch
+    first, then v)."""
+    w = np.arange(1, n + 1, dtype=np.float64) ** (-1.0 / (gamma - 1.0))
+    w *= mean_degree / w.mean()
+    p = w / w.sum()
+    m = int(n * mean_degree / 2)
+    rng = np.random.default_rng(seed)
+    u = rng.choice(n, size=m, p=p)
+    v = rng.choice(n, size=m, p=p)
+    return u, v, n
+
+
+def from_pairs(u, v, n):
+    """graph.py:111-148 from_edges: drop self-loops, symmetrise, deduplicate,
+    columns sorted within each row.  Returns (row_offsets, col_indices)."""
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    keep = u != v
+    u, v = u[keep], v[keep]
+    a = sp.coo_matrix((np.ones(u.size, dtype=np.int8), (u, v)), shape=(n, n)).tocsr()
+    a = (a + a.T).tocsr()
+    a.sum_duplicates()
+    a.sort_indices()
+    return a.indptr.astype(np.int64), a.indices.astype(np.int64)
+
+
+def largest_component(row_offsets, col_indices, n, original_ids=None):
+    """graph.py:232-261: the largest connected component, ties to the one
+    holding the smallest id (the reference labels components in order of
+    their smallest node), relabelled contiguously in increasing id order.
+    Returns (row_offsets, col_indices, original_ids)."""
+    from scipy.sparse.csgraph import connected_components
+
+    if original_ids is None:
+        original_ids = np.arange(n, dtype=np.int64)
+    a = sp.csr_matrix((np.ones(len(col_indices), dtype=np.int8), col_indices, row_offsets), shape=(n, n))
+    count, labels = connected_components(a, directed=False)
+    if count == 1:
+        return np.asarray(row_offsets), np.asarray(col_indices), np.asarray(original_ids)
+    sizes = np.bincount(labels, minlength=count)
+    first = np.full(count, n, dtype=np.int64)
+    np.minimum.at(first, labels, np.arange(n))
+    big = np.flatnonzero(sizes == sizes.max())
+    best = big[np.argmin(first[big])]
+    keep = np.flatnonzero(labels == best)
+    sub = a[keep][:, keep].tocsr()
+    sub.sort_indices()
+    return sub.indptr.astype(np.int64), sub.indices.astype(np.int64), np.asarray(original_ids)[keep].copy()
+
+
+def spectral_norm(a, tol=1e-7, max_iter=10000):
+    """graph.py:264-297: power iteration on A @ A from the uniform positive
+    vector; returns ||A v|| of the final unit iterate."""
+    n = a.shape[0]
+    if a.nnz == 0:
+        return 0.0
+    v = np.full(n, 1.0 / np.sqrt(n))
+    last = 0.0
+    for _ in range(max_iter):
+        w = a @ (a @ v)
+        est = np.sqrt(v @ w)
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0
+        v = w / nw
+        if abs(est - last) <= tol * max(est, 1e-300):
+            return float(np.linalg.norm(a @ v))
+        last = est
+    raise RuntimeError(f"spectral norm estimate did not settle in {max_iter} iterations")
+
+
+def config_csr(cfg, seed=0):
+    """(row_offsets, col_indices, original_ids) of a BASELINE config graph
+    after the largest component: cfg1 Chung-Lu 10^4, cfg2 R-MAT 18,
+    cfg3 R-MAT 22, proxy16 R-MAT 16."""
+    if cfg == "cfg1":
+        u, v, n = chung_lu_pairs(seed=seed)
+    else:
+        u, v, n = rmat_pairs({"proxy16": 16, "cfg2": 18, "cfg3": 22}[cfg], seed=seed)
+    off, col = from_pairs(u, v, n)
+    del u, v
+    return largest_component(off, col, n)
+
+
+def sample_queries(id_map, count, seed=0):
+    """cli.py:119-120: sort(default_rng(seed).choice(id_map, count, replace=False))."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(np.asarray(id_map), size=count, replace=False))
+
+
+# BASELINE.json per-config query batch, top-k and tolerance (the bench's
+# reference arm reads them here; tests check they equal generators.CONFIGS)
+BENCH_CONFIGS = {
+    "cfg1": dict(b=16, k=20, tol=1e-8),
+    "proxy16": dict(b=64, k=50, tol=1e-8),
+    "cfg2": dict(b=64, k=50, tol=1e-8),
+    "cfg3": dict(b=256, k=100, tol=1e-8),
+}

@@ -80,6 +80,8 @@ class KzTopkArgs(ctypes.Structure):
         ("ids_out", ctypes.c_void_p),
         ("vals_out", ctypes.c_void_p),
         ("count_out", ctypes.c_void_p),
+        ("bound_vals", ctypes.c_void_p),
+        ("bound_ids", ctypes.c_void_p),
     ]
 
 
@@ -166,6 +168,9 @@ def _declare(lib):
     lib.kz_last_error.restype = c.c_char_p
     lib.kz_version.restype = c.c_int
     lib.kz_launch_count.restype = c.c_longlong
+    lib.kz_num_sms.restype = c.c_int
+    lib.kz_k1_timing.argtypes = [c.c_int]
+    lib.kz_k1_timing_read.argtypes = [c.POINTER(c.c_double), c.POINTER(c.c_longlong)]
     lib.kz_graph_create.argtypes = [i64, i64, i64, vp, vp, c.POINTER(vp)]
     lib.kz_graph_destroy.argtypes = [vp]
     lib.kz_graph_info.argtypes = [vp] + [c.POINTER(i64)] * 5
@@ -178,7 +183,10 @@ def _declare(lib):
     lib.kz_topk_workspace_bytes.argtypes = [i32, i64, i32]
     lib.kz_topk_workspace_bytes.restype = sz
     lib.kz_topk_batch.argtypes = [c.POINTER(KzTopkArgs), vp, sz, vp]
-    lib.kz_coldot.argtypes = [i64, i32, vp, vp, vp, vp]
+    lib.kz_coldot.argtypes = [i64, i32, vp, vp, vp, vp, sz, vp]
+    lib.kz_coldot_workspace_bytes.argtypes = [i64, i32]
+    lib.kz_coldot_workspace_bytes.restype = sz
+    lib.kz_vec_op.argtypes = [i32, i64, dbl, vp, dbl, vp, vp, vp]
     lib.kz_profile_gather.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp, i32, vp]
     lib.kz_pearson_rerank.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp]
     lib.kz_graph_create_weighted.argtypes = [i64, i64, i64, vp, vp, vp, c.POINTER(vp)]
@@ -234,6 +242,18 @@ def torch_cuda():
 
 def stream_ptr(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def coldot(torch, lib, x, y, out, n, b=1, stream=None):
+    """out[j] = X[:, j] . Y[:, j] (kz_coldot) with this thread's scratch."""
+    ws = Workspace.get(torch, lib.kz_coldot_workspace_bytes(n, b), slot="coldot")
+    check(lib.kz_coldot(n, b, ptr(x), ptr(y), ptr(out), ptr(ws), ws.numel(),
+                        stream if stream is not None else stream_ptr(torch)))
+
+
+def vec_op(torch, lib, op, n, a, x, b, y, out):
+    """kz_vec_op: op 0 out = a*x + b*y (separately rounded), op 1 out = x / a."""
+    check(lib.kz_vec_op(op, n, float(a), ptr(x), float(b), ptr(y), ptr(out), stream_ptr(torch)))
 
 
 def ptr(t):

@@ -599,7 +599,7 @@ inline int stream_ctas_per_chunk(int64_t rows, int C, int nchunks) {
     const int vec = C >= 2 ? 2 : 1;
     const int64_t pairs = rows * C / vec;
     int64_t nb = (pairs + kThreads * 4 - 1) / (kThreads * 4);
-    const int64_t cap = std::max<int64_t>(1, (2 * kMaxCtasPerChunk + nchunks - 1) / nchunks);
+    const int64_t cap = std::max<int64_t>(1, (2 * max_ctas_per_chunk() + nchunks - 1) / nchunks);
     nb = std::max<int64_t>(1, std::min<int64_t>(nb, cap));
     return static_cast<int>(nb);
 }

@@ -171,7 +171,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
 
     const unsigned sgrid = static_cast<unsigned>(nchunks) * nb;
     const unsigned tgrid = static_cast<unsigned>(std::min<int64_t>(
-        static_cast<int64_t>(kMaxCtasPerChunk) * 2, ((n + 63) / 64) * nchunks));
+        static_cast<int64_t>(max_ctas_per_chunk()) * 2, ((n + 63) / 64) * nchunks));
 
     // right-hand side
     if (a->rhs) {
@@ -230,7 +230,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
             KZ_LAUNCH_CHECK();
         }
         const int64_t ntiles = (n + kLrRows - 1) / kLrRows;
-        const unsigned lgrid = static_cast<unsigned>(std::min<int64_t>(KZ_LR_MINBLOCKS * kNumSMs, ntiles));
+        const unsigned lgrid = static_cast<unsigned>(std::min<int64_t>(KZ_LR_MINBLOCKS * num_sms(), ntiles));
         for (int j0 = 0; j0 < w.bpad; j0 += 8 * nt) {
 #define KZ_LR(NN)                                                                                              \
     do {                                                                                                       \
@@ -338,7 +338,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         // a solve that needs iteration H folds x once and continues in place
         if (hist && !folded && k >= w.H) {
             if (int rc = hist_coef(w.H - 1)) return rc;
-            const unsigned fgrid = static_cast<unsigned>(std::min<int64_t>(8 * kMaxCtasPerChunk, (static_cast<int64_t>(blk_elems) + 255) / 256));
+            const unsigned fgrid = static_cast<unsigned>(std::min<int64_t>(8 * max_ctas_per_chunk(), (static_cast<int64_t>(blk_elems) + 255) / 256));
             KZ_DISPATCH_C(C, cg_hist_fold_kernel<CC><<<fgrid, 256, 0, st>>>(w.x, history(), n, nchunks); ::kz::note_launch());
             KZ_LAUNCH_CHECK();
             folded = true;
@@ -415,7 +415,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         oh = history();
     }
     if (a->perm) {
-        invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
+        invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * max_ctas_per_chunk(), (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
         ::kz::note_launch();
         KZ_DISPATCH_C(C, store_gather_kernel<CC><<<tgrid, kThreads, 0, st>>>(a->scores, w.x, n, n * CC, b, nchunks, w.iperm, a->clamp, oh); ::kz::note_launch());
     } else {
@@ -504,38 +504,57 @@ extern "C" int kz_eigen_batch(const kz_eigen* h, const kz_cg_args* a, void* ws, 
     return cg_batch_impl(h->op, a, ws, ws_bytes, stream, h);
 }
 
+extern "C" size_t kz_coldot_workspace_bytes(int64_t n, int32_t b) {
+    if (n < 1 || b < 1) return 256;
+    const size_t nb = static_cast<size_t>(stream_ctas_per_chunk(n, 1, b));
+    return ((sizeof(double) * static_cast<size_t>(b) * nb + 255) & ~size_t(255)) + sizeof(int32_t) * b + 256;
+}
+
 extern "C" int kz_coldot(int64_t n, int32_t b, const double* X, const double* Y, double* out,
-                         void* stream) {
+                         void* ws, size_t ws_bytes, void* stream) {
     clear_error();
     if (n < 1 || b < 1 || !X || !Y || !out) return fail(KZ_EARG, "bad coldot arguments");
+    if (!ws || ws_bytes < kz_coldot_workspace_bytes(n, b)) return fail(KZ_EARG, "workspace too small");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // column-major == chunk width 1, one chunk per column
     const int nb = stream_ctas_per_chunk(n, 1, b);
+    Carver cv(ws, ws_bytes);
     RedScratch red;
     red.nb = nb;
-    static thread_local double* part = nullptr;
-    static thread_local int32_t* cnt = nullptr;
-    static thread_local size_t cap = 0, capb = 0;
-    const size_t need = static_cast<size_t>(b) * nb;
-    if (need > cap) {
-        if (part) cudaFree(part);
-        part = nullptr;
-        cap = 0;
-        KZ_CUDA(cudaMalloc(&part, sizeof(double) * need));
-        cap = need;
-    }
-    if (static_cast<size_t>(b) > capb) {
-        if (cnt) cudaFree(cnt);
-        cnt = nullptr;
-        capb = 0;
-        KZ_CUDA(cudaMalloc(&cnt, sizeof(int32_t) * b));
-        capb = b;
-    }
-    red.part = part;
-    red.cnt = cnt;
-    KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * b, st));
+    red.part = cv.take<double>(static_cast<size_t>(b) * nb);
+    red.cnt = cv.take<int32_t>(b);
+    KZ_CUDA(cudaMemsetAsync(red.cnt, 0, sizeof(int32_t) * b, st));
     SolveState s;
     coldot_kernel<1><<<static_cast<unsigned>(b) * nb, kThreads, 0, st>>>(X, Y, n, n, n, red, FIN_WRITE, s, out, 0); ::kz::note_launch();
+    KZ_LAUNCH_CHECK();
+    return KZ_OK;
+}
+
+// out = a*x + b*y (y may be NULL: out = a*x) with separately rounded products
+// and sum -- numpy's `x += a*p`, `r -= a*q`, `p = r + beta*p` bit for bit;
+// op 1: out = x / a (numpy's `w / nw`).
+__global__ void vec_op_kernel(int op, int64_t n, double a, const double* x, double b, const double* y,
+                              double* out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (op == 1) {
+            out[i] = __ddiv_rn(x[i], a);
+        } else {
+            const double ax = __dmul_rn(a, x[i]);
+            out[i] = y ? __dadd_rn(ax, __dmul_rn(b, y[i])) : ax;
+        }
+    }
+}
+
+extern "C" int kz_vec_op(int32_t op, int64_t n, double a, const double* x, double b, const double* y,
+                         double* out, void* stream) {
+    clear_error();
+    if (n < 0 || !x || !out || (op != 0 && op != 1)) return fail(KZ_EARG, "bad vec_op arguments");
+    if (n == 0) return KZ_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(4 * max_ctas_per_chunk(), (n + 255) / 256));
+    vec_op_kernel<<<grid, 256, 0, st>>>(op, n, a, x, b, y, out);
+    ::kz::note_launch();
     KZ_LAUNCH_CHECK();
     return KZ_OK;
 }

@@ -14,6 +14,12 @@ int fail(int code, const std::string& msg);  // records msg, returns code
 void clear_error();
 void note_launch();  // counts every kernel launch of the library (kz_launch_count)
 void add_launches(long long n);
+// K1 launch timing for bench.py (kz_k1_timing): when enabled, every K1
+// launch outside stream capture is bracketed by two CUDA events on its
+// own stream; kz_k1_timing_read sums their elapsed times.
+bool k1_timing_on();
+void k1_timing_begin(cudaStream_t st, cudaEvent_t* e0);
+void k1_timing_end(cudaStream_t st, cudaEvent_t e0);
 
 #define KZ_CUDA(call)                                                                   \
     do {                                                                                \
@@ -33,8 +39,10 @@ void add_launches(long long n);
 
 constexpr int kThreads = 256;        // threads per CTA for the streaming kernels
 constexpr int kWarps = kThreads / 32;
-constexpr int kNumSMs = 148;         // B200
-constexpr int kMaxCtasPerChunk = kNumSMs * 8;
+// SM count of the current device (148 on B200), queried once per device;
+// every persistent grid is sized from it.
+int num_sms();
+inline int max_ctas_per_chunk() { return num_sms() * 8; }
 
 // Bump allocator over a caller-provided workspace (256-byte aligned slices).
 struct Carver {

@@ -512,7 +512,7 @@ inline void dense_plan(int64_t M, int64_t K, int& mtiles, int& ksplit, int64_t& 
                        int64_t rows_tile = kDenseRows) {
     mtiles = static_cast<int>((M + rows_tile - 1) / rows_tile);
     const int64_t kblocks = (K + kDenseK - 1) / kDenseK;
-    int64_t want = (4 * kNumSMs + mtiles - 1) / mtiles;  // ~4 CTAs per SM
+    int64_t want = (4 * num_sms() + mtiles - 1) / mtiles;  // ~4 CTAs per SM
     want = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, kblocks), kDenseMaxSplit));
     kper = ((kblocks + want - 1) / want) * kDenseK;
     ksplit = static_cast<int>((K + kper - 1) / kper);

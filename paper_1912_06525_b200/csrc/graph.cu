@@ -1,6 +1,8 @@
 // graph.cu -- operator handles (kz_graph) and the K1 SpMM entry point.
 #include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -21,6 +23,57 @@ void clear_error() { g_last_error.clear(); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int num_sms() {
+    static std::mutex mu;
+    static std::vector<int> cache;  // per device ordinal
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 148;  // B200; only reached without a usable device
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= static_cast<int>(cache.size())) cache.resize(dev + 1, 0);
+    if (cache[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 148;
+        }
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
+// ---- K1 launch timing (kz_k1_timing / kz_k1_timing_read) ----
+static std::atomic<bool> g_k1_timing{false};
+static std::mutex g_k1_mu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_k1_events;
+
+bool k1_timing_on() { return g_k1_timing.load(std::memory_order_relaxed); }
+void k1_timing_begin(cudaStream_t st, cudaEvent_t* e0) {
+    *e0 = nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    if (cudaEventCreate(e0) != cudaSuccess) {
+        cudaGetLastError();
+        *e0 = nullptr;
+        return;
+    }
+    cudaEventRecord(*e0, st);
+}
+void k1_timing_end(cudaStream_t st, cudaEvent_t e0) {
+    if (!e0) return;
+    cudaEvent_t e1 = nullptr;
+    if (cudaEventCreate(&e1) != cudaSuccess) {
+        cudaGetLastError();
+        cudaEventDestroy(e0);
+        return;
+    }
+    cudaEventRecord(e1, st);
+    std::lock_guard<std::mutex> lock(g_k1_mu);
+    g_k1_events.emplace_back(e0, e1);
+}
+
 }  // namespace kz
 
 using namespace kz;
@@ -28,6 +81,33 @@ using namespace kz;
 extern "C" const char* kz_last_error(void) { return g_last_error.c_str(); }
 extern "C" long long kz_launch_count(void) { return g_launches.load(); }
 extern "C" int kz_version(void) { return 1; }
+
+extern "C" int kz_k1_timing(int enable) {
+    std::lock_guard<std::mutex> lock(g_k1_mu);
+    for (auto& p : g_k1_events) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    g_k1_events.clear();
+    g_k1_timing.store(enable != 0);
+    return KZ_OK;
+}
+
+extern "C" int kz_k1_timing_read(double* total_ms, long long* launches) {
+    std::lock_guard<std::mutex> lock(g_k1_mu);
+    double tot = 0.0;
+    for (auto& p : g_k1_events) {
+        KZ_CUDA(cudaEventSynchronize(p.second));
+        float ms = 0.f;
+        KZ_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = static_cast<long long>(g_k1_events.size());
+    return KZ_OK;
+}
+
+extern "C" int kz_num_sms(void) { return num_sms(); }
 
 namespace {
 
@@ -94,7 +174,7 @@ void build_schedule(const std::vector<int64_t>& rp, int64_t rows, int64_t cols, 
     max_deg = 0;
     // granularity: aim for >= ~2 work units per resident warp of one chunk pass
     const double est_total = static_cast<double>(rp[rows]) + 4.0 * static_cast<double>(rows);
-    const double unit = std::max(64.0, std::min(kGroupCost, est_total / (2.0 * kNumSMs * kSpmmMinBlocks * kWarps)));
+    const double unit = std::max(64.0, std::min(kGroupCost, est_total / (2.0 * num_sms() * kSpmmMinBlocks * kWarps)));
     // hub segments no longer than a work unit (at least 1,024): large
     // operators get kSegLen, small ones keep short segments so one hub row
     // does not become a serial tail
@@ -309,7 +389,7 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
             return fail(KZ_EOOM, "validation flag");
         }
         cudaMemset(bad, 0, sizeof(int32_t));
-        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (nnz + 255) / 256));
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(4 * max_ctas_per_chunk(), (nnz + 255) / 256));
         check_cols_kernel<<<grid, 256>>>(g->colidx, nnz, static_cast<int32_t>(cols), bad);
         note_launch();
         int32_t h = 0;

@@ -65,8 +65,8 @@ extern "C" int kz_connected_components(int64_t n, int64_t nnz, const int32_t* sr
     int32_t* hchanged = nullptr;
     KZ_CUDA(cudaMalloc(&changed, sizeof(int32_t)));
     KZ_CUDA(cudaHostAlloc(&hchanged, sizeof(int32_t), cudaHostAllocDefault));
-    const unsigned gn = static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (n + 255) / 256));
-    const unsigned ge = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(8 * kMaxCtasPerChunk, (nnz + 255) / 256)));
+    const unsigned gn = static_cast<unsigned>(std::min<int64_t>(4 * max_ctas_per_chunk(), (n + 255) / 256));
+    const unsigned ge = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(8 * max_ctas_per_chunk(), (nnz + 255) / 256)));
     cc_init<<<gn, 256, 0, st>>>(labels, n);
     note_launch();
     int rc = KZ_OK;

@@ -7,13 +7,16 @@
 // with the query's reference profile (0 when either has zero variance,
 // clipped to [-1, 1]; linkpred.py:197-204), then a bitonic sort by
 // (corr desc, Katz score desc, id asc) -- lexsort((top, -score, -corr)).
+#include <algorithm>
+
 #include "spmm.cuh"
 
 using namespace kz;
 
 namespace {
 
-constexpr int kMaxCand = 2048;
+// candidates one CTA sorts in shared memory (20 bytes each, dynamic smem)
+constexpr int kMaxCand = 8192;
 
 // out[j][slot][c] = S[src][top[j][c]] for each triple (src, j, slot)
 __global__ void profile_gather_kernel(const double* __restrict__ S, int64_t n,
@@ -37,9 +40,12 @@ __global__ void __launch_bounds__(kThreads)
                           double* __restrict__ corr_out, int64_t* __restrict__ order_out) {
     const int j = blockIdx.x;
     const int m = count[j];
-    __shared__ double sc[kMaxCand];
-    __shared__ double ss[kMaxCand];
-    __shared__ int si[kMaxCand];
+    int P = 1;
+    while (P < m) P <<= 1;
+    extern __shared__ double dsm[];
+    double* sc = dsm;        // [P]
+    double* ss = dsm + P;    // [P]
+    int* si = reinterpret_cast<int*>(dsm + 2 * P);  // [P]
     __shared__ double s_rm, s_sr;
     const double* r = ref + static_cast<size_t>(j) * T1;
     if (threadIdx.x == 0) {
@@ -72,8 +78,7 @@ __global__ void __launch_bounds__(kThreads)
         si[c] = c;
         corr_out[static_cast<size_t>(j) * s + c] = cr;
     }
-    int P = 1;
-    while (P < m) P <<= 1;
+    if (!order_out) return;  // correlations only (the caller orders them)
     for (int c = m + threadIdx.x; c < P; c += blockDim.x) {
         sc[c] = -INFINITY;
         ss[c] = -INFINITY;
@@ -117,7 +122,7 @@ extern "C" int kz_profile_gather(const double* S, int64_t n, int32_t ntrip, cons
     if (ntrip < 0 || !S || (ntrip > 0 && !trip) || !top_ids || !counts || !profiles || s < 1 || T1 < 1)
         return fail(KZ_EARG, "bad profile gather arguments");
     if (ntrip == 0) return KZ_OK;
-    const int grid = std::min(ntrip, kMaxCtasPerChunk * 2);
+    const int grid = std::min(ntrip, max_ctas_per_chunk() * 2);
     profile_gather_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(S, n, trip, ntrip, top_ids, counts, s, profiles, T1); ::kz::note_launch();
     KZ_LAUNCH_CHECK();
     return KZ_OK;
@@ -128,10 +133,16 @@ extern "C" int kz_pearson_rerank(const double* profiles, const double* ref, cons
                                  int32_t T1, int32_t s, double* corr_out, int64_t* order_out,
                                  void* stream) {
     clear_error();
-    if (b < 1 || T1 < 2 || s < 1 || s > kMaxCand || !profiles || !ref || !top_ids || !top_scores ||
-        !counts || !corr_out || !order_out)
+    if (b < 1 || T1 < 2 || s < 1 || !profiles || !ref || !top_ids || !top_scores || !counts || !corr_out)
         return fail(KZ_EARG, "bad rerank arguments");
-    pearson_rerank_kernel<<<b, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    if (order_out && s > kMaxCand)
+        return fail(KZ_EARG, "rerank sorts at most 8192 candidates per query (pass order_out = NULL for correlations only)");
+    int P = 1;
+    while (P < std::min(s, kMaxCand)) P <<= 1;
+    const size_t smem = order_out ? static_cast<size_t>(P) * 20 : 0;
+    KZ_CUDA(cudaFuncSetAttribute(pearson_rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(8192 * 20)));
+    pearson_rerank_kernel<<<b, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(
         profiles, ref, top_ids, top_scores, counts, T1, s, corr_out, order_out); ::kz::note_launch();
     KZ_LAUNCH_CHECK();
     return KZ_OK;

@@ -42,6 +42,9 @@ struct kz_lrc {
     const double* u = nullptr;      // n2 x ldl row-major
     const double* udT = nullptr;    // ell x ld2 row-major, (U diag(d))^T
     int64_t ld2 = 0, ldl = 0;       // leading dimensions, rounded up to even (zero padded)
+    // every sigma < 1: the preconditioner exists (factor.py:329-330); only
+    // the calls that apply it (query, lrc_pcg, PRECOND) raise otherwise
+    bool spectrum_ok = true;
 };
 
 namespace {
@@ -181,7 +184,7 @@ struct LrcCtx {
     cudaStream_t st;
     int C, nch;
     unsigned egrid(int64_t rows) const {
-        return static_cast<unsigned>(std::min<int64_t>(2 * kMaxCtasPerChunk, (rows * C * nch + 255) / 256 + 1));
+        return static_cast<unsigned>(std::min<int64_t>(2 * max_ctas_per_chunk(), (rows * C * nch + 255) / 256 + 1));
     }
 
     int spmm(const kz_graph* g, const double* Xg, int64_t ldxg, const double* Xs, int64_t ldxs,
@@ -270,9 +273,11 @@ extern "C" int kz_lrc_create(const kz_lrc_desc* d, kz_lrc** out) {
     if (!d->full || (d->n1 > 0 && d->n2 > 0 && (!d->a12 || !d->a21)) || (d->n1 > 0 && !d->minv) ||
         (d->n2 > 0 && (!d->a22 || !d->linv || !d->linvT)) || (d->ell > 0 && (!d->u || !d->udT || !d->sigma)))
         return fail(KZ_EARG, "missing LRC operand");
+    bool spectrum_ok = true;
     for (int64_t i = 0; i < d->ell; ++i)
-        if (!(d->sigma[i] < 1.0)) return fail(KZ_ESPECTRUM, "correction eigenvalue at or above 1");
+        if (!(d->sigma[i] < 1.0)) spectrum_ok = false;
     auto* h = new kz_lrc();
+    h->spectrum_ok = spectrum_ok;
     h->n = d->n;
     h->n1 = d->n1;
     h->n2 = d->n2;
@@ -317,6 +322,7 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
     if (!mode_pcg && !a->qpos) return fail(KZ_EARG, "need qpos or f");
     if (!a->out || !a->reports) return fail(KZ_EARG, "NULL outputs");
     if (mode_pcg && h->n2 == 0) return fail(KZ_EARG, "empty separator");
+    if (!h->spectrum_ok) return fail(KZ_ESPECTRUM, "correction eigenvalue at or above 1");
     const int b = a->b;
     const int C = lrc_chunk(a);
     if (!chunk_ok(C)) return fail(KZ_EARG, "bad chunk width");
@@ -354,7 +360,7 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
     KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nch, st));
     KZ_CUDA(cudaMemsetAsync(w.ds.cnt, 0, sizeof(int32_t) * w.ds.cnt_cap, st));
     if (int rc = zero_spmm_counters(w.dims, nch, w.sp, st)) return rc;
-    const unsigned tg = static_cast<unsigned>(std::min<int64_t>(2 * kMaxCtasPerChunk, ((n + 63) / 64) * nch));
+    const unsigned tg = static_cast<unsigned>(std::min<int64_t>(2 * max_ctas_per_chunk(), ((n + 63) / 64) * nch));
     int rc = KZ_OK;
 
     if (!mode_pcg) {
@@ -475,7 +481,7 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
             return rc;
         if ((rc = cx.coldot(w.rhs, ln, w.rhs, ln, n, FIN_WRITE, w.resid2, 0))) return rc;
         if (a->perm) {
-            invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * kMaxCtasPerChunk, (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
+            invert_perm_kernel<<<static_cast<unsigned>(std::min<int64_t>(4 * max_ctas_per_chunk(), (n + 255) / 256)), 256, 0, st>>>(a->perm, w.iperm, n);
             note_launch();
             KZ_DISPATCH_C(C, store_gather_kernel<CC><<<tg, kThreads, 0, st>>>(a->out, w.kk, n, ln, b, nch, w.iperm,
                                                                               a->clamp);
@@ -549,6 +555,7 @@ extern "C" int kz_lrc_apply(const kz_lrc* h, int32_t op, int32_t b, const double
         case KZ_LRC_SCHUR:
             return cx.schur(in1, n2, out, nullptr, nullptr);
         case KZ_LRC_PRECOND:
+            if (!h->spectrum_ok) return fail(KZ_ESPECTRUM, "correction eigenvalue at or above 1");
             return cx.precond(in1, n2, out, n2);
         case KZ_LRC_SCHUR_RHS: {
             if (!in2) return fail(KZ_EARG, "schur_rhs needs g2");

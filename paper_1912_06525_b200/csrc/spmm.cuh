@@ -699,7 +699,7 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
         const int v = e ? std::atoi(e) : kSpmmMinBlocks;
         return v >= 1 && v <= kSpmmMinBlocks ? v : kSpmmMinBlocks;
     }();
-    const int64_t cap = static_cast<int64_t>(kNumSMs) * ctas_per_sm;
+    const int64_t cap = static_cast<int64_t>(num_sms()) * ctas_per_sm;
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cap, (total + kWarps - 1) / kWarps)));
     a.nchunks = nchunks;
     a.nwarps = static_cast<int32_t>(grid) * kWarps;
@@ -710,6 +710,8 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
     if (a.ldd == 0) a.ldd = g->rows * C;
     a.vals = g->vals;
     const bool w = g->vals != nullptr;
+    cudaEvent_t tev = nullptr;
+    if (k1_timing_on()) k1_timing_begin(st, &tev);
     // experiments: KZ_K1_CARVEOUT = preferred shared-memory carveout (percent)
     static const int carveout = [] {
         const char* e = std::getenv("KZ_K1_CARVEOUT");
@@ -734,9 +736,12 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
         KZ_SPMM_CASE(16)
         KZ_SPMM_CASE(32)
         KZ_SPMM_CASE(64)
-        default: return fail(KZ_EARG, "unsupported chunk width");
+        default:
+            if (tev) cudaEventDestroy(tev);
+            return fail(KZ_EARG, "unsupported chunk width");
     }
 #undef KZ_SPMM_CASE
+    if (tev) k1_timing_end(st, tev);
     note_launch();
     KZ_LAUNCH_CHECK();
     return KZ_OK;

@@ -68,7 +68,21 @@ struct MaskRef {
     const int32_t* colidx;
     const int64_t* rows;    // device [b], -1 = none
     const int64_t* self;    // device [b], -1 = none
+    // exclusive upper bound on the key (score, id) per column: elements at or
+    // above (bval[j], bid[j]) are left out -- the continuation pass of a
+    // top-k larger than one candidate buffer (bid[j] < 0 = no bound)
+    const double* bval;     // device [b] or null
+    const int64_t* bid;     // device [b] or null
 };
+
+__device__ __forceinline__ bool above_bound(const MaskRef& m, int j, unsigned long long hi, unsigned int lo) {
+    if (!m.bid) return false;
+    const int64_t id = m.bid[j];
+    if (id < 0) return false;
+    const unsigned long long bhi = score_key(m.bval[j]);
+    const unsigned int blo = ~static_cast<unsigned int>(id);
+    return hi > bhi || (hi == bhi && lo >= blo);
+}
 
 __device__ __forceinline__ bool is_masked(const MaskRef& m, int j, int64_t id) {
     if (m.self && m.self[j] == id) return true;
@@ -99,7 +113,7 @@ __global__ void topk_init_kernel(ColState* cs, int b, int64_t n, int k) {
 // per-column histogram of the next digit among elements matching the prefix
 __global__ void __launch_bounds__(kThreads)
     topk_hist_kernel(const double* __restrict__ scores, int64_t n, int slices,
-                     const ColState* __restrict__ cs, unsigned int* __restrict__ hist) {
+                     const ColState* __restrict__ cs, unsigned int* __restrict__ hist, MaskRef m) {
     const int j = blockIdx.x / slices, sl = blockIdx.x % slices;
     const ColState c = cs[j];
     if (c.done) return;
@@ -113,7 +127,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
         const unsigned long long hi = score_key(col[i]);
         const unsigned int lo = ~static_cast<unsigned int>(i);
-        if (cmp_prefix(hi, lo, c, c.shift) == 0) atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
+        if (cmp_prefix(hi, lo, c, c.shift) == 0 && !above_bound(m, j, hi, lo)) atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
     }
     __syncthreads();
     unsigned int* gh = hist + static_cast<size_t>(j) * kBins;
@@ -134,7 +148,7 @@ __global__ void topk_mask_kernel(const double* __restrict__ scores, int64_t n,
     auto visit = [&](int64_t id) {
         const unsigned long long hi = score_key(col[id]);
         const unsigned int lo = ~static_cast<unsigned int>(id);
-        if (cmp_prefix(hi, lo, c, c.shift) == 0) atomicSub(gh + digit_of(hi, lo, ns), 1u);
+        if (cmp_prefix(hi, lo, c, c.shift) == 0 && !above_bound(m, j, hi, lo)) atomicSub(gh + digit_of(hi, lo, ns), 1u);
     };
     const int64_t self = m.self ? m.self[j] : -1;
     if (threadIdx.x == 0 && self >= 0) visit(self);
@@ -221,7 +235,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
         const unsigned long long hi = score_key(col[i]);
         const unsigned int lo = ~static_cast<unsigned int>(i);
-        if (cmp_prefix(hi, lo, c, c.shift) >= 0 && !is_masked(m, j, i)) {
+        if (cmp_prefix(hi, lo, c, c.shift) >= 0 && !above_bound(m, j, hi, lo) && !is_masked(m, j, i)) {
             const int pos = atomicAdd(&cs[j].ncand, 1);
             if (pos < kCap) {
                 ckey[static_cast<size_t>(j) * kCap + pos] = hi;
@@ -324,7 +338,9 @@ extern "C" int kz_topk_batch(const kz_topk_args* a, void* ws, size_t ws_bytes, v
         !a->count_out)
         return fail(KZ_EARG, "bad top-k arguments");
     if (a->n >= (int64_t(1) << 31) - 1) return fail(KZ_EARG, "n too large");
-    if (std::min<int64_t>(a->k, a->n) > kCap) return fail(KZ_EARG, "k above the supported 4096");
+    if (std::min<int64_t>(a->k, a->n) > kCap)
+        return fail(KZ_EARG, "k above 4096 per pass (continue with bound_vals/bound_ids)");
+    if ((a->bound_vals == nullptr) != (a->bound_ids == nullptr)) return fail(KZ_EARG, "bound needs values and ids");
     if (!ws || ws_bytes < kz_topk_workspace_bytes(a->b, a->n, a->k)) return fail(KZ_EARG, "workspace too small");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Carver cv(ws, ws_bytes);
@@ -342,16 +358,18 @@ extern "C" int kz_topk_batch(const kz_topk_args* a, void* ws, size_t ws_bytes, v
         KZ_CUDA(cudaMemcpyAsync(w.mself, a->self_ids, sizeof(int64_t) * b, cudaMemcpyHostToDevice, st));
         m.self = w.mself;
     }
+    m.bval = a->bound_vals;
+    m.bid = a->bound_ids;
     KZ_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(unsigned int) * b * kBins, st));
     topk_init_kernel<<<(b + 127) / 128, 128, 0, st>>>(w.cs, b, a->n, a->k); ::kz::note_launch();
     KZ_LAUNCH_CHECK();
     // slices per column: ~64k elements each, enough CTAs to fill the chip
     int slices = static_cast<int>((a->n + 65535) / 65536);
-    slices = std::max(slices, static_cast<int>(std::min<int64_t>((2 * kMaxCtasPerChunk + b - 1) / b,
+    slices = std::max(slices, static_cast<int>(std::min<int64_t>((2 * max_ctas_per_chunk() + b - 1) / b,
                                                                   (a->n + 4095) / 4096)));
     slices = std::max(slices, 1);
     for (int r = 0; r < kRounds; ++r) {
-        topk_hist_kernel<<<static_cast<unsigned>(b) * slices, kThreads, 0, st>>>(a->scores, a->n, slices, w.cs, w.hist); ::kz::note_launch();
+        topk_hist_kernel<<<static_cast<unsigned>(b) * slices, kThreads, 0, st>>>(a->scores, a->n, slices, w.cs, w.hist, m); ::kz::note_launch();
         topk_mask_kernel<<<b, kThreads, 0, st>>>(a->scores, a->n, w.cs, w.hist, m); ::kz::note_launch();
         topk_select_kernel<<<b, kThreads, 0, st>>>(w.cs, w.hist); ::kz::note_launch();
         KZ_LAUNCH_CHECK();

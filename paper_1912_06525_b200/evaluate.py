@@ -14,6 +14,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import threading
+
 import numpy as np
 
 from .graph import Graph, from_edges, largest_connected_component
@@ -101,19 +103,48 @@ def _pair_bucket(dataset):
     return pb
 
 
-def rank_lists(idx, method, queries, pool, T=None, tol=1e-10, batch=256):
-    """Ranked candidate ids (original) for every query, in query order."""
-    out = []
-    for s0 in range(0, len(queries), batch):
-        qs = np.asarray(queries[s0 : s0 + batch], dtype=np.int64)
+def rank_lists(idx, method, queries, pool, T=None, tol=1e-10, batch=256, workers=1):
+    """Ranked candidate ids (original) for every query, in query order.
+
+    Queries are answered in blocks of `batch` (one batched device call per
+    block).  With workers > 1 the blocks run on that many host threads, each
+    on its own CUDA stream, over the one shared index (the reference's
+    ThreadPoolExecutor fan-out, linkpred.py:309-317).  The block composition
+    does not depend on `workers`, so every query's result -- and every
+    statistic built from them -- is identical for any worker count."""
+    def rank_block(qs):
         if method == "katz":
             preds = katz_rank_batch(idx, qs, pool, tol=tol)
         elif method == "sparse-katz":
             preds = sparse_katz_batch(idx, qs, pool, T=T, tol=tol)
         else:
             raise ValueError(f"unknown method {method!r}")
-        out.extend([c for c, _ in p.candidates] for p in preds)
-    return out
+        return [[c for c, _ in p.candidates] for p in preds]
+
+    blocks = [np.asarray(queries[s0 : s0 + batch], dtype=np.int64) for s0 in range(0, len(queries), batch)]
+    if workers <= 1 or len(blocks) <= 1:
+        return [lst for qs in blocks for lst in rank_block(qs)]
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _lib
+
+    torch = _lib.torch_cuda()
+    idx.operator(), idx.mask_operator()  # create the shared device state once, up front
+    local = threading.local()
+    caller = torch.cuda.current_stream()
+
+    def run(qs):
+        st = getattr(local, "stream", None)
+        if st is None:
+            st = local.stream = torch.cuda.Stream()
+        st.wait_stream(caller)
+        with torch.cuda.stream(st):
+            out = rank_block(qs)
+        st.synchronize()
+        return out
+
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return [lst for res in ex.map(run, blocks) for lst in res]
 
 
 def _stat(recalls):
@@ -149,10 +180,12 @@ def evaluate_recall(idx, method, dataset, s, T=None, query_sample=None, pool=Non
     return {label: _stat(r) for label, r in per.items()}
 
 
-def evaluate_recall_sweep(idx, methods, dataset, s_values, T=None, query_sample=None, tol=1e-10, workers=1):
+def evaluate_recall_sweep(idx, methods, dataset, s_values, T=None, query_sample=None, tol=1e-10, workers=1,
+                          batch=256):
     """Recall@s for several methods and sizes from one ranking per query
-    (linkpred.py:282-337).  `workers` is accepted for API compatibility; the
-    queries are batched on the device instead of fanned out over threads."""
+    (linkpred.py:282-337).  `workers` > 1 answers the query blocks on that
+    many threads and CUDA streams (rank_lists); the statistics do not depend
+    on it (reference tests/test_linkpred.py:355-365)."""
     if not dataset.positives:
         raise EmptyPositivesError("no positive pairs to evaluate")
     s_values = sorted(set(int(s) for s in s_values))
@@ -165,7 +198,7 @@ def evaluate_recall_sweep(idx, methods, dataset, s_values, T=None, query_sample=
     rows = []
     for method in methods:
         per = {(label, s): [] for label in ("overall", *BUCKET_LABELS) for s in s_values}
-        ranked = rank_lists(idx, method, queries, pool, T, tol)
+        ranked = rank_lists(idx, method, queries, pool, T, tol, batch=batch, workers=workers)
         for u, lst in zip(queries, ranked):
             mine = partners[u]
             by_label = {label: {v for v in mine if pb[(u, v) if u < v else (v, u)] == label}

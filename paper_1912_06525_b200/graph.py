@@ -390,7 +390,7 @@ def spectral_norm(g, tol=1e-7, max_iter=10000, op=None):
     st = _lib.stream_ptr(torch)
 
     def dot(x, y):
-        _lib.check(lib.kz_coldot(n, 1, _lib.ptr(x), _lib.ptr(y), _lib.ptr(out), st))
+        _lib.coldot(torch, lib, x, y, out, n, 1, st)
         return float(out.item())
 
     last = 0.0
@@ -401,8 +401,7 @@ def spectral_norm(g, tol=1e-7, max_iter=10000, op=None):
         nw = np.sqrt(dot(w, w))
         if nw == 0.0:
             return 0.0
-        v = w / nw
-        w = torch.empty_like(v)
+        _lib.vec_op(torch, lib, 1, n, nw, w, 0.0, None, v)  # v = w / nw
         if abs(est - last) <= tol * max(est, 1e-300):
             op.spmm(v, t, b=1)
             return float(np.sqrt(dot(t, t)))

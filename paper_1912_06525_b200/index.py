@@ -23,6 +23,7 @@ from __future__ import annotations
 import hashlib
 import os
 import struct
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -74,15 +75,37 @@ class BlockPartition:
         return self.perm[self.n1 :]
 
 
+# guards the lazy device uploads below: an index is shared by concurrent
+# query threads, and the first callers must not race to create
+# (and leak) two copies of one operator
+_DEV_LOCK = threading.RLock()
+
+
 class _DeviceGraphMixin:
     """Lazily uploaded device state shared by both index kinds."""
 
     def _op_cache(self):
         cache = self.__dict__.get("_dev")
         if cache is None:
-            cache = {}
-            self.__dict__["_dev"] = cache
+            with _DEV_LOCK:
+                cache = self.__dict__.setdefault("_dev", {})
         return cache
+
+    def _cached(self, key, make):
+        """cache[key], created once under the lock; the upload is complete on
+        the device before any thread (on any stream) sees it."""
+        cache = self._op_cache()
+        val = cache.get(key)
+        if val is None:
+            with _DEV_LOCK:
+                val = cache.get(key)
+                if val is None:
+                    val = make()
+                    from . import _lib
+
+                    _lib.torch_cuda().cuda.current_stream().synchronize()
+                    cache[key] = val
+        return val
 
     def internal_id(self, original):
         pos = int(np.searchsorted(self.id_map, original))
@@ -198,41 +221,37 @@ class KatzIndex(_DeviceGraphMixin):
 
     def operator(self):
         """Device operator of A in partition order (the solve order)."""
-        cache = self._op_cache()
-        if "op" not in cache:
+        def make():
             off, col = self.adjacency_permuted()
-            cache["op"] = DeviceOperator(off, col.astype(np.int32), self.n)
-        return cache["op"]
+            return DeviceOperator(off, col.astype(np.int32), self.n)
+        return self._cached("op", make)
 
     def mask_operator(self):
         """Device operator of A in internal order (neighbour masks for top-k)."""
-        cache = self._op_cache()
-        if "mask" not in cache:
+        def make():
             off, col = self.adjacency_internal()
-            cache["mask"] = DeviceOperator(off, col.astype(np.int32), self.n)
-        return cache["mask"]
+            return DeviceOperator(off, col.astype(np.int32), self.n)
+        return self._cached("mask", make)
 
     def solve_positions(self, internal):
         """Positions of internal ids in the solve (partition) order."""
         return self.bp.inv_perm[np.asarray(internal, dtype=np.int64)]
 
     def device_perm(self):
-        cache = self._op_cache()
-        if "perm" not in cache:
+        def make():
             from . import _lib
 
             torch = _lib.torch_cuda()
-            cache["perm"] = torch.as_tensor(self.bp.perm, dtype=torch.int64).cuda()
-        return cache["perm"]
+            return torch.as_tensor(self.bp.perm, dtype=torch.int64).cuda()
+        return self._cached("perm", make)
 
     def lrc(self):
         """Device LRC operands (lazily uploaded; see lrc.py)."""
-        cache = self._op_cache()
-        if "lrc" not in cache:
+        def make():
             from .lrc import DeviceLRC
 
-            cache["lrc"] = DeviceLRC(self)
-        return cache["lrc"]
+            return DeviceLRC(self)
+        return self._cached("lrc", make)
 
     # -- reference methods, evaluated on the device -------------------------
     def apply_m_permuted(self, x):
@@ -309,25 +328,23 @@ class GraphIndex(_DeviceGraphMixin):
 
     def operator(self):
         """Device operator in the solve order."""
-        cache = self._op_cache()
-        if "op" not in cache:
+        def make():
             g = self.graph
             if self._order is None:
-                cache["op"] = DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
-            else:
-                off, col = permute_csr(g.row_offsets, g.col_indices, self._order, self._inv)
-                cache["op"] = DeviceOperator(off, col, g.n)
-        return cache["op"]
+                return DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
+            off, col = permute_csr(g.row_offsets, g.col_indices, self._order, self._inv)
+            return DeviceOperator(off, col, g.n)
+        return self._cached("op", make)
 
     def mask_operator(self):
         """Device operator in internal order (neighbour masks for top-k)."""
         if self._order is None:
             return self.operator()
-        cache = self._op_cache()
-        if "mask" not in cache:
+
+        def make():
             g = self.graph
-            cache["mask"] = DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
-        return cache["mask"]
+            return DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), g.n)
+        return self._cached("mask", make)
 
     def solve_positions(self, internal):
         internal = np.asarray(internal, dtype=np.int64)
@@ -340,13 +357,13 @@ class GraphIndex(_DeviceGraphMixin):
     def device_perm(self):
         if self._order is None:
             return None
-        cache = self._op_cache()
-        if "perm" not in cache:
+
+        def make():
             from . import _lib
 
             torch = _lib.torch_cuda()
-            cache["perm"] = torch.as_tensor(self._order, dtype=torch.int64).cuda()
-        return cache["perm"]
+            return torch.as_tensor(self._order, dtype=torch.int64).cuda()
+        return self._cached("perm", make)
 
     def adjacency_internal(self):
         return self.graph.row_offsets, self.graph.col_indices

@@ -45,38 +45,65 @@ def pearson(x, y):
     return float(np.clip((xc @ yc) / (sx * sy), -1.0, 1.0))
 
 
+_TOPK_PASS = 4096  # entries per column one kz_topk_batch call returns
+_RERANK_SMEM = 8192  # candidates kz_pearson_rerank orders in shared memory
+
+
 def topk_device(scores, k, mask_op=None, mask_rows=None, self_ids=None):
     """K4 masked top-k over the columns of scores (cuda fp64 [b][n]).
 
     Returns (ids int64 [b][k], vals fp64 [b][k], counts int32 [b]) on the
-    device; ids are positions in the scores' order (internal ids)."""
+    device; ids are positions in the scores' order (internal ids).  A k above
+    4096 runs in passes: each continues below the last key of the previous
+    one (kz_topk_args.bound_*), so any k up to n is exact."""
     torch = _lib.torch_cuda()
     lib = _lib.load()
     b, n = scores.shape
     k = int(k)
     ids = torch.empty((b, k), dtype=torch.int64, device="cuda")
     vals = torch.empty((b, k), dtype=torch.float64, device="cuda")
-    counts = torch.empty((b,), dtype=torch.int32, device="cuda")
-    args = _lib.KzTopkArgs()
-    args.b = b
-    args.k = k
-    args.n = n
-    args.scores = scores.data_ptr()
+    counts = torch.zeros((b,), dtype=torch.int32, device="cuda")
     keep = []
+    margs = {}
     if mask_op is not None and mask_rows is not None:
-        args.mask_graph = mask_op.handle.value
         arr, p = _lib.i64_array(mask_rows)
         keep.append(arr)
-        args.mask_rows = p
+        margs["mask_graph"], margs["mask_rows"] = mask_op.handle.value, p
     if self_ids is not None:
         arr, p = _lib.i64_array(self_ids)
         keep.append(arr)
-        args.self_ids = p
-    args.ids_out = ids.data_ptr()
-    args.vals_out = vals.data_ptr()
-    args.count_out = counts.data_ptr()
-    ws = _lib.Workspace.get(torch, lib.kz_topk_workspace_bytes(b, n, k), slot="topk")
-    _lib.check(lib.kz_topk_batch(ctypes.byref(args), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(torch)))
+        margs["self_ids"] = p
+    st = _lib.stream_ptr(torch)
+    bval = bid = None
+    for k0 in range(0, k, _TOPK_PASS):
+        kk = min(_TOPK_PASS, k - k0)
+        pi = ids if kk == k else torch.empty((b, kk), dtype=torch.int64, device="cuda")
+        pv = vals if kk == k else torch.empty((b, kk), dtype=torch.float64, device="cuda")
+        pc = counts if kk == k else torch.empty((b,), dtype=torch.int32, device="cuda")
+        args = _lib.KzTopkArgs()
+        args.b, args.k, args.n = b, kk, n
+        args.scores = scores.data_ptr()
+        for name, v in margs.items():
+            setattr(args, name, v)
+        args.ids_out, args.vals_out, args.count_out = pi.data_ptr(), pv.data_ptr(), pc.data_ptr()
+        if bid is not None:
+            args.bound_vals, args.bound_ids = bval.data_ptr(), bid.data_ptr()
+        ws = _lib.Workspace.get(torch, lib.kz_topk_workspace_bytes(b, n, kk), slot="topk")
+        _lib.check(lib.kz_topk_batch(ctypes.byref(args), _lib.ptr(ws), ws.numel(), st))
+        if kk == k:
+            break
+        ids[:, k0 : k0 + kk] = pi
+        vals[:, k0 : k0 + kk] = pv
+        counts += pc
+        # continue strictly below each column's last key; a column that came
+        # up short has nothing left (its next passes return 0 entries)
+        last = (pc.to(torch.int64) - 1).clamp(min=0).unsqueeze(1)
+        bval = torch.gather(pv, 1, last).squeeze(1).contiguous()
+        bid = torch.where(pc > 0, torch.gather(pi, 1, last).squeeze(1), torch.full_like(pc, -1, dtype=torch.int64))
+        # an exhausted column must return nothing more: bound it at the
+        # smallest possible key (score 0, id n-1)
+        bid = torch.where(pc < kk, torch.full_like(bid, n - 1), bid).contiguous()
+        bval = torch.where(pc < kk, torch.zeros_like(bval), bval).contiguous()
     return ids, vals, counts
 
 
@@ -165,9 +192,18 @@ def sparse_katz_batch(idx, qs, s, T=None, tol=1e-10, anchor_batch=256):
                                          T1, st))
         del a_scores
     corr = torch.empty((b, s_eff), dtype=torch.float64, device="cuda")
-    order = torch.empty((b, s_eff), dtype=torch.int64, device="cuda")
+    big = s_eff > _RERANK_SMEM
+    order = None if big else torch.empty((b, s_eff), dtype=torch.int64, device="cuda")
     _lib.check(lib.kz_pearson_rerank(_lib.ptr(profiles), _lib.ptr(ref), _lib.ptr(top), _lib.ptr(top_vals),
                                      _lib.ptr(counts), b, T1, s_eff, _lib.ptr(corr), _lib.ptr(order), st))
+    if big:
+        # more candidates than one CTA sorts in shared memory: the same
+        # lexsort((top, -score, -corr)) as three stable device sorts
+        valid = torch.arange(s_eff, device="cuda").unsqueeze(0) < counts.unsqueeze(1)
+        key_c = torch.where(valid, -corr, torch.full_like(corr, float("inf")))
+        order = torch.argsort(top, dim=1, stable=True)
+        order = torch.gather(order, 1, torch.argsort(torch.gather(-top_vals, 1, order), dim=1, stable=True))
+        order = torch.gather(order, 1, torch.argsort(torch.gather(key_c, 1, order), dim=1, stable=True))
     top_h, corr_h, order_h, counts_h = (top.cpu().numpy(), corr.cpu().numpy(), order.cpu().numpy(),
                                         counts.cpu().numpy())
     out = []

@@ -220,6 +220,10 @@ class DeviceLRC:
                              dtype=torch.float64).cuda().reshape(1, -1).contiguous()
         if ft.shape[1] != self.n2:
             raise ValueError("right-hand side has the wrong length")
+        if self.n2 == 0:  # solver.py:127-152 with an empty system: x = [], converged at 0 iterations
+            x = torch.zeros(0, dtype=torch.float64, device="cuda")
+            rep = SolveReport(iterations=0, final_residual_norm=0.0, converged=True, wall_time=0.0)
+            return (x.cpu().numpy() if as_numpy else x), rep
         out, reps, ms = self._run(1, f=ft, tol=tol, max_iter=max_iter, start_seed=start_seed,
                                   clamp=False, out_rows=self.n2)
         r = reps[0]
@@ -257,6 +261,10 @@ class DeviceLRC:
         return self._apply(3, v, None, self.n2)
 
     def apply_schur(self, v):
+        if self.n2 == 0:
+            if np.size(v) != 0:
+                raise ValueError("vector has the wrong length")
+            return np.zeros(0)
         return self._apply(0, v, None, self.n2)
 
     def apply_precond(self, r):

@@ -255,8 +255,13 @@ def cg(apply_a, b, tol=1e-8, max_iter=None, start_seed=None):
 def _dot(torch, x, y):
     lib = _lib.load()
     out = torch.empty(1, dtype=torch.float64, device="cuda")
-    _lib.check(lib.kz_coldot(x.numel(), 1, _lib.ptr(x), _lib.ptr(y), _lib.ptr(out), _lib.stream_ptr(torch)))
+    _lib.coldot(torch, lib, x, y, out, x.numel())
     return float(out.item())
+
+
+def _axpby(torch, a, x, b, y, out):
+    """out = a*x + b*y on the device (kz_vec_op; numpy's rounding)."""
+    _lib.vec_op(torch, _lib.load(), 0, x.numel(), a, x, b, y, out)
 
 
 def _generic_cg(apply_a, bt, tol, max_iter, start_seed, as_numpy, torch):
@@ -273,14 +278,16 @@ def _generic_cg(apply_a, bt, tol, max_iter, start_seed, as_numpy, torch):
     thresh = tol * np.sqrt(_dot(torch, bt, bt))
     if start_seed is None:
         x = torch.zeros_like(bt)
-        r = bt.clone()
+        r = torch.empty_like(bt)
+        _axpby(torch, 1.0, bt, 0.0, None, r)  # r = b
     else:
         x = torch.as_tensor(_start_vector(n, start_seed), dtype=torch.float64).cuda()
         r = bt - apply(x)
     rnorm = np.sqrt(_dot(torch, r, r))
     it = 0
     if rnorm > thresh:
-        p = r.clone()
+        p = torch.empty_like(r)
+        _axpby(torch, 1.0, r, 0.0, None, p)  # p = r
         rs = _dot(torch, r, r)
         while it < max_iter:
             q = apply(p)
@@ -288,14 +295,14 @@ def _generic_cg(apply_a, bt, tol, max_iter, start_seed, as_numpy, torch):
             if pq <= 0.0:
                 raise RuntimeError("operator is not positive definite")
             a = rs / pq
-            x += a * p
-            r -= a * q
+            _axpby(torch, a, p, 1.0, x, x)  # x += a*p
+            _axpby(torch, -a, q, 1.0, r, r)  # r -= a*q
             it += 1
             rs_new = _dot(torch, r, r)
             rnorm = np.sqrt(rs_new)
             if rnorm <= thresh:
                 break
-            p = r + (rs_new / rs) * p
+            _axpby(torch, rs_new / rs, p, 1.0, r, p)  # p = r + (rs_new/rs)*p
             rs = rs_new
     rep = SolveReport(iterations=it, final_residual_norm=float(rnorm),
                       converged=bool(rnorm <= thresh), wall_time=time.perf_counter() - t0)

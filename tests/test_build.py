@@ -328,3 +328,78 @@ def test_device_factor_helpers_match_oracle(gpu, name):
     rv = li @ (m12.T @ np.linalg.solve(dense_m11, m12 @ (li.T @ v)))
     got = gpu.apply_correction(ref.dc, ref.m12, ref.bc, v)
     assert np.linalg.norm(got - rv) <= 1e-11 * max(1.0, np.linalg.norm(rv))
+
+
+# ---- BASELINE config 4: the beta x ell sweep on the R-MAT 16 proxy ----
+CFG4 = os.path.join(GOLDEN, "cfg4_ref.npz")
+CFG4_COMBOS = [(bf, ell) for bf in (0.1, 0.5, 0.9, 0.99) for ell in (32, 128)]
+
+
+@pytest.fixture(scope="module")
+def cfg4():
+    from oracle import katz_oracle as O
+
+    off, col, ids = O.config_csr("proxy16")
+    return O, O.csr_matrix(off, col, len(ids)), ids, np.load(CFG4)
+
+
+def _cfg4_ref_scores(O, a, ids, rec, k, method):
+    """The reference's scores: the oracle's tol=1e-14 solve + the stored
+    float32 deviation (tests/golden/make_cfg4.py)."""
+    dev = rec[f"{k}_{method}_dev"].astype(np.float64)
+    qi = np.searchsorted(ids, rec[f"{k}_queries"][: dev.shape[0]])
+    ex = np.array([O.query_cg_csr(a, float(rec[f"{k}_alpha"]), int(q), tol=1e-14)[0] for q in qi])
+    return ex + dev
+
+
+@pytest.mark.parametrize("bf,ell", CFG4_COMBOS)
+def test_cfg4_oracle_cg_matches_reference(cfg4, bf, ell):
+    """The oracle's CSR restatement of query_cg_baseline reproduces the
+    reference's iterations and scores at every beta of the sweep (the pin of
+    the oracle at cfg4)."""
+    O, a, ids, rec = cfg4
+    k = f"b{bf:g}_l{ell}"
+    alpha = float(rec[f"{k}_alpha"])
+    want = _cfg4_ref_scores(O, a, ids, rec, k, "cg")
+    qi = np.searchsorted(ids, rec[f"{k}_queries"])
+    for j, q in enumerate(qi):
+        x, rep = O.query_cg_csr(a, alpha, int(q), tol=1e-8)
+        assert rep.iterations == int(rec[f"{k}_cg_iters"][j])
+        assert rep.converged == bool(rec[f"{k}_cg_conv"][j])
+        if j < want.shape[0]:
+            assert np.linalg.norm(x - want[j]) <= 1e-12 * np.linalg.norm(want[j])
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("bf,ell", CFG4_COMBOS)
+def test_cfg4_device_build_lrc_and_cg_match_reference(gpu, cfg4, bf, ell):
+    """BASELINE config 4 on the proxy (SURVEY §8(c) pin for the cfg2/cfg4 LRC
+    side): the device build at beta*lambda in {0.1, 0.5, 0.9, 0.99} and
+    ell in {32, 128} reproduces the reference build's correction
+    eigenvalues, and its LRC (query) and plain-CG (query_cg_baseline)
+    answers match the reference's: iterations +/-1 on 4 queries, rel L2
+    <= 1e-10 on the stored score columns."""
+    import warnings
+
+    from paper_1912_06525_b200.generators import config_graph
+
+    O, a, ids, rec = cfg4
+    k = f"b{bf:g}_l{ell}"
+    g = config_graph("proxy16")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        idx = gpu.build_index(g, alpha=float(rec[f"{k}_alpha"]), ell=ell, seed=0,
+                              spectral_norm=float(rec[f"{k}_spectral_norm"]))
+    assert idx.n2 == int(rec[f"{k}_n2"])
+    assert np.allclose(idx.lr.values, rec[f"{k}_sigma"], rtol=0, atol=1e-9)
+    qs = rec[f"{k}_queries"]
+    for method, fn in (("lrc", gpu.query_batch), ("cg", gpu.query_cg_baseline_batch)):
+        scores, reps = fn(idx, qs, tol=1e-8)
+        for j in range(len(qs)):
+            assert abs(reps[j].iterations - int(rec[f"{k}_{method}_iters"][j])) <= 1
+            assert reps[j].converged == bool(rec[f"{k}_{method}_conv"][j])
+        want = _cfg4_ref_scores(O, a, ids, rec, k, method)
+        for j in range(want.shape[0]):
+            assert np.linalg.norm(scores[j] - want[j]) <= 1e-10 * np.linalg.norm(want[j]), (method, j)
+    del idx

@@ -368,3 +368,83 @@ print("graphs ok")
     env = dict(os.environ, KZ_GRAPHS="1")
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "graphs ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_topk_above_one_pass_matches_lexsort(torch, kz):
+    """k beyond one kz_topk_batch pass (4,096 per column): the continuation
+    passes (bound_vals / bound_ids) give exactly np.lexsort's order,
+    including heavy ties across pass boundaries and columns with fewer
+    unmasked entries than k."""
+    rng = np.random.default_rng(9)
+    b, n = 3, 20_000
+    S = np.abs(rng.standard_normal((b, n)))
+    S[0, ::3] = 0.5  # ties that straddle the 4,096 boundaries
+    S[2, : n - 5000] = 0.0  # long run of equal zeros
+    Sd = torch.as_tensor(S).cuda()
+    self_ids = np.array([1, 2, 3])
+    for k in (4096, 4097, 9000, n - 1, n + 10):
+        ids, vals, counts = kz.topk_device(Sd, k, None, None, self_ids)
+        ids, vals, counts = ids.cpu().numpy(), vals.cpu().numpy(), counts.cpu().numpy()
+        for j in range(b):
+            cand = np.array([i for i in range(n) if i != self_ids[j]])
+            order = cand[np.lexsort((cand, -S[j][cand]))][:k]
+            assert counts[j] == len(order)
+            assert np.array_equal(ids[j][: len(order)], order)
+            assert np.array_equal(vals[j][: len(order)], S[j][order])
+            assert np.all(ids[j][len(order):] == -1)
+
+
+def test_katz_rank_with_s_above_one_topk_pass(torch, kz):
+    """katz_rank with s > 4,096 candidates equals the oracle's
+    _candidate_order (linkpred.py:145-152) at full length."""
+    rec, n = chunglu_fixture()
+    g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"], original_ids=np.arange(n))
+    beta = float(rec["beta"])
+    idx = kz.GraphIndex(g, beta)
+    a = O.csr_matrix(rec["row_offsets"], rec["col_indices"], n)
+    q = int(rec["queries"][0])
+    s = n  # every candidate
+    pred = kz.katz_rank_batch(idx, [q], s, tol=1e-12)[0]
+    x, _ = O.query_cg_csr(a, beta, q, tol=1e-12)
+    want = O.candidate_order(n, x, q, a.indices[a.indptr[q] : a.indptr[q + 1]], s)
+    got = np.array([c for c, _ in pred.candidates])
+    assert len(got) == len(want)
+    nx = np.linalg.norm(x)
+    diff = np.flatnonzero(got != want)
+    assert np.all(np.abs(x[got[diff]] - x[want[diff]]) <= 1e-12 * nx)
+
+
+def test_sparse_katz_rerank_device_sort_fallback(torch, kz, monkeypatch):
+    """Above 8,192 candidates the rerank order comes from stable device sorts
+    instead of the shared-memory bitonic sort; both give the same
+    lexsort((top, -score, -corr)) order (forced here on a small case)."""
+    from paper_1912_06525_b200 import linkpred
+
+    idx = kz.load_index(os.path.join(GOLDEN, "ba300.klrc"))
+    qs = idx.id_map[::11][:8]
+    want = [p.candidates for p in kz.sparse_katz_batch(idx, qs, 40)]
+    monkeypatch.setattr(linkpred, "_RERANK_SMEM", 4)
+    got = [p.candidates for p in kz.sparse_katz_batch(idx, qs, 40)]
+    assert got == want
+
+
+def test_vec_op_rounds_like_numpy(torch, kz):
+    """kz_vec_op (the generic cg() updates) rounds the products and the sum
+    separately, as numpy's x += a*p, r -= a*q, p = r + b*p do."""
+    from paper_1912_06525_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    n = 100_003
+    x, y = rng.standard_normal(n), rng.standard_normal(n)
+    a, b = 0.3721931, -1.77e-3
+    xt, yt = torch.as_tensor(x).cuda(), torch.as_tensor(y).cuda()
+    out = torch.empty_like(xt)
+    _lib.vec_op(torch, lib, 0, n, a, xt, 1.0, yt, out)
+    assert np.array_equal(out.cpu().numpy(), y + a * x)
+    _lib.vec_op(torch, lib, 0, n, -a, xt, 1.0, yt, out)
+    assert np.array_equal(out.cpu().numpy(), y - a * x)
+    _lib.vec_op(torch, lib, 0, n, b, xt, 1.0, yt, out)
+    assert np.array_equal(out.cpu().numpy(), y + b * x)
+    _lib.vec_op(torch, lib, 1, n, 7.25, xt, 0.0, None, out)
+    assert np.array_equal(out.cpu().numpy(), x / 7.25)

@@ -182,3 +182,41 @@ def test_spectrum_error(kz):
     bad.lr = lr
     with pytest.raises(kz.SpectrumError):
         kz.query(bad, int(idx.id_map[0]))
+
+
+def test_spectrum_error_only_where_the_preconditioner_is_applied(kz):
+    """SpectrumError comes from apply_approx_schur_inverse (factor.py:329-330),
+    so query / lrc_pcg raise it, while apply_schur and schur_rhs -- which
+    never read sigma (solver.py:104-115) -- still answer."""
+    import copy
+
+    idx, _, ix = case(kz, "er40")
+    bad = copy.copy(idx)
+    bad.__dict__.pop("_dev", None)
+    lr = copy.copy(idx.lr)
+    lr.values = lr.values.copy()
+    lr.values[0] = 1.0
+    bad.lr = lr
+    rng = np.random.default_rng(2)
+    v = rng.standard_normal(idx.n2)
+    assert rel(kz.apply_schur(bad, v), O.apply_schur(ix, v)) <= 1e-12
+    g1, g2 = rng.standard_normal(idx.n1), rng.standard_normal(idx.n2)
+    assert rel(kz.schur_rhs(bad, g1, g2), O.schur_rhs(ix, g1, g2)) <= 1e-12
+    with pytest.raises(kz.SpectrumError):
+        kz.lrc_pcg(bad, v)
+    with pytest.raises(kz.SpectrumError):
+        kz.query(bad, int(idx.id_map[0]))
+
+
+@pytest.mark.parametrize("name", ["k2", "p4", "star5"])
+def test_lrc_pcg_on_an_empty_separator(kz, name):
+    """n2 == 0: the reference's lrc_pcg returns an empty x with a converged,
+    0-iteration report (solver.py:127-158 on an empty system); apply_schur
+    of an empty vector is empty."""
+    idx, _, _ = case(kz, name)
+    assert idx.n2 == 0
+    x, rep = kz.lrc_pcg(idx, np.zeros(0))
+    assert x.shape == (0,)
+    assert rep.iterations == 0 and rep.converged and rep.final_residual_norm == 0.0
+    assert kz.apply_schur(idx, np.zeros(0)).shape == (0,)
+    assert kz.schur_rhs(idx, np.zeros(idx.n1), np.zeros(0)).shape == (0,)
