@@ -31,6 +31,12 @@ struct SolveState {
     int32_t* n_active = nullptr;      // [1]
     int32_t* err = nullptr;           // [1]
     int32_t* iter_dev = nullptr;      // [1] iteration number for graph replay (NULL: host-passed)
+    // residual-history CG (cg.cu): the convergence finalize records each
+    // column's step length a_k and direction coefficient beta_k of
+    // iterations 1..hist_len into [hist_len][bpad] (pre-zeroed)
+    double* ahist = nullptr;
+    double* bhist = nullptr;
+    int32_t hist_len = 0;
 };
 
 // The iteration number a kernel of the solve loop works on: passed by the
@@ -100,6 +106,11 @@ __device__ __forceinline__ void finalize_chunk(int mode, const SolveState& s, do
                 } else {
                     s.betac[col] = v / s.rs[col];
                     s.rs[col] = v;
+                }
+                if (s.ahist && iter <= s.hist_len) {
+                    const size_t h = static_cast<size_t>(iter - 1) * s.bpad + col;
+                    s.ahist[h] = s.alpha[col];
+                    s.bhist[h] = s.active[col] ? s.betac[col] : 0.0;
                 }
             }
             act = s.active[col] != 0;
@@ -224,7 +235,7 @@ __global__ void __launch_bounds__(kThreads)
     cg_update_kernel(double* __restrict__ r, const double* __restrict__ q, int64_t rows,
                      int64_t ldr, int64_t ldq, RedScratch red, int mode, SolveState s, int iter,
                      const int32_t* __restrict__ cnt = nullptr, double beta = 0.0,
-                     double* __restrict__ r_out = nullptr) {
+                     double* __restrict__ r_out = nullptr, double* __restrict__ q_out = nullptr) {
     constexpr int VEC = Cfg<C>::SVEC;
     const int chunk = blockIdx.x / red.nb, local = blockIdx.x - chunk * red.nb;
     iter = cur_iter(s, iter);
@@ -234,6 +245,9 @@ __global__ void __launch_bounds__(kThreads)
     if (cnt) cnt += static_cast<size_t>(chunk) * ldq;
     // history mode: r_{k+1} goes to its own slot, r_k stays for the final x
     double* __restrict__ ro = r_out ? r_out + static_cast<size_t>(chunk) * ldr : r;
+    // sparse first iteration of the q-recurrence: q0 (formed from the counts)
+    // is kept for the next iteration's q1 = M r1 + beta_0 q0
+    double* __restrict__ qo = q_out ? q_out + static_cast<size_t>(chunk) * ldq : nullptr;
     const size_t npairs = static_cast<size_t>(rows) * C / VEC;
     const size_t stride = static_cast<size_t>(red.nb) * kThreads;
     const size_t t0 = static_cast<size_t>(local) * kThreads + threadIdx.x;
@@ -258,6 +272,7 @@ __global__ void __launch_bounds__(kThreads)
                 const int32_t c = __ldcs(cnt + pi * VEC + k);
                 qv[k] = __dadd_rn(rv[k], __dmul_rn(-beta, __dmul_rn(beta, static_cast<double>(c))));
             }
+            if (qo) st_plain<VEC>(qo + pi * VEC, qv);
         } else {
             ld_plain<VEC>(q + pi * VEC, qv);
         }
@@ -451,15 +466,39 @@ static __global__ void cg_hist_coef_kernel(const double* __restrict__ ahist, con
     }
 }
 
-// x = x_0 + sum_i c_i r_i over the whole chunked block (the fold)
+// x = x_0 + sum_i c_i r_i over the whole chunked block (the fold); with
+// p_out also the current direction p = sum_i d_i r_i (dcoef [H][bpad],
+// cg_hist_dcoef_kernel), which the q-recurrence never materialises
 template <int C>
-__global__ void cg_hist_fold_kernel(double* __restrict__ x, CgHistory h, int64_t rows, int nchunks) {
+__global__ void cg_hist_fold_kernel(double* __restrict__ x, CgHistory h, int64_t rows, int nchunks,
+                                    double* __restrict__ p_out = nullptr, const double* __restrict__ dcoef = nullptr,
+                                    int nd = 0) {
     const size_t total = static_cast<size_t>(nchunks) * rows * C;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int c = static_cast<int>(e % C);
         const int chunk = static_cast<int>(e / (static_cast<size_t>(rows) * C));
-        x[e] = hist_value(h, e, chunk * C + c);
+        const int col = chunk * C + c;
+        x[e] = hist_value(h, e, col);
+        if (p_out) {
+            double v = 0.0;
+            for (int i = 0; i < nd; ++i) v = fma(dcoef[static_cast<size_t>(i) * h.bpad + col], h.slots[i * h.slot + e], v);
+            p_out[e] = v;
+        }
+    }
+}
+
+// d_i of the direction p_{m-1} = r_{m-1} + beta_{m-2} p_{m-2} = sum_{i<m} d_i r_i
+// (d_{m-1} = 1, d_i = beta_i d_{i+1}; p_0 = r_0)
+static __global__ void cg_hist_dcoef_kernel(const double* __restrict__ bhist, int m, int bpad,
+                                            double* __restrict__ dcoef) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= bpad) return;
+    double d = 1.0;
+    dcoef[static_cast<size_t>(m - 1) * bpad + col] = d;
+    for (int i = m - 2; i >= 0; --i) {
+        d *= bhist[static_cast<size_t>(i) * bpad + col];
+        dcoef[static_cast<size_t>(i) * bpad + col] = d;
     }
 }
 

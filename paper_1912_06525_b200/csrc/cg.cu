@@ -4,7 +4,23 @@
 // column runs the recurrence of cg() (solver.py:62-101) exactly -- the same
 // scalar formulas, the same stop test ||r|| <= tol*||b||, the same
 // non-positive-curvature error -- and is frozen (masked) once it stops, so
-// its iteration count is its own.  Per iteration three kernels run:
+// its iteration count is its own.
+//
+// Residual-history form (the default whenever H >= 3 residual blocks fit):
+// the direction p is never materialised.  With q_k = M p_k, M = I - beta A,
+// p_k = r_k + b_{k-1} p_{k-1} gives the q-recurrence
+//   q_k = M r_k + b_{k-1} q_{k-1},      p_k.q_k = r_k.q_k
+// (the second by M-conjugacy of p_k and p_{k-1}; in exact arithmetic both are
+// the reference's quantities, so a_k = rs_k / (p_k.q_k) and the stop tests
+// are the reference's).  Per iteration two kernels run:
+//   spmm   q = M r + b*q (in place, per-column b), dots r.q, a = rs / r.q
+//   update r_{k+1} = r_k - a*q into its own slot, r.r, stop test, b = rs'/rs
+// and x = x_0 + sum_i c_i r_i is formed once at the end from the kept
+// residuals (CgHistory) -- 6 block passes per iteration instead of 8.  A
+// solve that outgrows the H slots folds x and p from them once and continues
+// with the direction form below.
+//
+// Direction form (small solves replayed as CUDA graphs, or H < 3):
 //   spmm   q = p - beta*A p, column dots p.q, step length a = rs/pq
 //   update r -= a*q, column dots r.r, stop test, beta_cg = rs_new/rs
 //   pupd   x += a*p (deferred from solver.py:87), p = r + beta_cg*p
@@ -34,7 +50,7 @@ struct CgWork {
     int C, nchunks, bpad, nb;
     int H = 0;             // residual-history slots (0: x updated every iteration)
     double *x, *r, *p, *q; // r = slot 0 of the H residual slots
-    double *ahist = nullptr, *bhist = nullptr, *coef = nullptr;  // [H][bpad]
+    double *ahist = nullptr, *bhist = nullptr, *coef = nullptr, *dcoef = nullptr;  // [H][bpad]
     int32_t* kcol = nullptr;                                     // [bpad]
     SpmmScratch sp;
     RedScratch red;
@@ -68,6 +84,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
         w.ahist = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
         w.bhist = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
         w.coef = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
+        w.dcoef = cv.take<double>(static_cast<size_t>(w.H) * w.bpad);
         w.kcol = cv.take<int32_t>(w.bpad);
     }
     carve_spmm_scratch(cv, g, w.nchunks, w.C, w.sp);
@@ -164,6 +181,11 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     if (hist) {
         KZ_CUDA(cudaMemsetAsync(w.ahist, 0, sizeof(double) * static_cast<size_t>(w.H) * w.bpad, st));
         KZ_CUDA(cudaMemsetAsync(w.bhist, 0, sizeof(double) * static_cast<size_t>(w.H) * w.bpad, st));
+        // the convergence finalize records a_k, b_k (iterations 1 .. H-1
+        // run in history mode; a fold at H switches to the direction form)
+        s.ahist = w.ahist;
+        s.bhist = w.bhist;
+        s.hist_len = w.H - 1;
     }
     // x0 = 0: the eigen start writes every x, a seeded start broadcasts it,
     // and the history form never reads an x it did not write
@@ -333,54 +355,17 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     const bool sparse_first_on = !(sf_env && sf_env[0] == '0');
     const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs &&
                               w.bpad <= 65535;  // one grid row per column in walk2_count_kernel
-    auto launch_iter = [&](int k) -> int {
-        // history mode for iterations 1 .. H-1: r_k -> slot k, no x update;
-        // a solve that needs iteration H folds x once and continues in place
-        if (hist && !folded && k >= w.H) {
-            if (int rc = hist_coef(w.H - 1)) return rc;
-            const unsigned fgrid = static_cast<unsigned>(std::min<int64_t>(8 * max_ctas_per_chunk(), (static_cast<int64_t>(blk_elems) + 255) / 256));
-            KZ_DISPATCH_C(C, cg_hist_fold_kernel<CC><<<fgrid, 256, 0, st>>>(w.x, history(), n, nchunks); ::kz::note_launch());
-            KZ_LAUNCH_CHECK();
-            folded = true;
-        }
-        const bool hmode = hist && !folded;
-        double* rin = hist ? (folded ? slot(w.H - 1) : slot(k - 1)) : w.r;
-        double* rout = hmode ? slot(k) : nullptr;
-        double* rcur = hmode ? rout : rin;  // r_k after this iteration's update
-        double* xk = hmode ? nullptr : w.x;
-        double* ah = hmode ? w.ahist + static_cast<size_t>(k - 1) * w.bpad : nullptr;
-        double* bh = hmode ? w.bhist + static_cast<size_t>(k - 1) * w.bpad : nullptr;
-        if (k == 1 && sparse_first) {
-            int32_t* cnt = reinterpret_cast<int32_t*>(w.q);
-            KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
-            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, g->max_deg))),
-                             static_cast<unsigned>(w.bpad));
-            KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
-                                                                                w.qpos, b);
-                          ::kz::note_launch());
-            KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_sparse_pq_kernel<CC><<<w.bpad, kThreads, 0, st>>>(rin, cnt, n * CC, g->rowptr,
-                                                                                  g->colidx, w.qpos, a->beta, s, k);
-                          ::kz::note_launch());
-            KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red,
-                                                                              FIN_CG_CONV, s, k, cnt, a->beta, rout);
-                          ::kz::note_launch());
-            KZ_LAUNCH_CHECK();
-            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh, hmode ? rin : nullptr); ::kz::note_launch());
-            KZ_LAUNCH_CHECK();
-            return KZ_OK;
-        }
-        const double* pin = hmode && k == 1 ? rin : w.p;  // p_0 = r_0 (slot 0) in history mode
+    auto k1_args = [&](const double* xin, const double* z, int k) {
         SpmmArgs sa = make_spmm_args(g, w.sp);
-        sa.Xg = pin;
-        sa.Xs = pin;
-        sa.Z = nullptr;
+        sa.Xg = xin;
+        sa.Xs = xin;
+        sa.Z = z;
         sa.Y = w.q;
         sa.s0 = 0.0;
+        sa.s0v = z ? s.betac : nullptr;  // q-recurrence: q = M r + b_{k-1} q
         sa.s1 = 1.0;
         sa.s2 = -a->beta;
-        sa.D = nullptr;
+        sa.D = nullptr;  // dots with Xs: p.q (direction form) or r.q (q-recurrence)
         sa.chunk_active = s.chunk_active;
         sa.want_dot = 1;
         sa.hook.mode = 1;
@@ -395,17 +380,91 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         sa.hook.n_active = s.n_active;
         sa.hook.iter = k;
         sa.hook.iter_dev = s.iter_dev;
-        if (int rc = launch_spmm(g, C, nchunks, sa, st)) return rc;
-        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k, nullptr, 0.0, rout); ::kz::note_launch());
+        return sa;
+    };
+    auto launch_iter = [&](int k) -> int {
+        // history mode (q-recurrence) for iterations 1 .. H-1: r_k -> slot k;
+        // a solve that needs iteration H folds x and the direction p from the
+        // slots once and continues in the direction form, in place
+        if (hist && !folded && k >= w.H) {
+            if (int rc = hist_coef(w.H - 1)) return rc;
+            cg_hist_dcoef_kernel<<<static_cast<unsigned>((w.bpad + 127) / 128), 128, 0, st>>>(w.bhist, w.H, w.bpad,
+                                                                                             w.dcoef);
+            ::kz::note_launch();
+            const unsigned fgrid = static_cast<unsigned>(std::min<int64_t>(8 * max_ctas_per_chunk(), (static_cast<int64_t>(blk_elems) + 255) / 256));
+            KZ_DISPATCH_C(C, cg_hist_fold_kernel<CC><<<fgrid, 256, 0, st>>>(w.x, history(), n, nchunks, w.p, w.dcoef,
+                                                                            w.H);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            folded = true;
+        }
+        if (hist && !folded) {
+            double* rin = slot(k - 1);
+            double* rout = slot(k);
+            if (k == 1 && sparse_first) {
+                // q0 = M r0 from the 2-walk counts (kept in p, unused in this
+                // form), p0.q0 over N(q); the update stores q0 for q1
+                int32_t* cnt = reinterpret_cast<int32_t*>(w.p);
+                KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
+                const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, g->max_deg))),
+                                 static_cast<unsigned>(w.bpad));
+                KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
+                                                                                    w.qpos, b);
+                              ::kz::note_launch());
+                KZ_LAUNCH_CHECK();
+                KZ_DISPATCH_C(C, cg_sparse_pq_kernel<CC><<<w.bpad, kThreads, 0, st>>>(rin, cnt, n * CC, g->rowptr,
+                                                                                      g->colidx, w.qpos, a->beta, s, k);
+                              ::kz::note_launch());
+                KZ_LAUNCH_CHECK();
+                KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, nullptr, n, n * CC, n * CC, w.red,
+                                                                                  FIN_CG_CONV, s, k, cnt, a->beta, rout,
+                                                                                  w.q);
+                              ::kz::note_launch());
+                KZ_LAUNCH_CHECK();
+                return KZ_OK;
+            }
+            // q_{k-1} = M r_{k-1} + b_{k-2} q_{k-2} (q0 = M r0), a = rs / r.q
+            if (int rc = launch_spmm(g, C, nchunks, k1_args(rin, k == 1 ? nullptr : w.q, k), st)) return rc;
+            KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red,
+                                                                              FIN_CG_CONV, s, k, nullptr, 0.0, rout);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            return KZ_OK;
+        }
+        // direction form: after a fold r lives in slot H-1 (updated in place)
+        double* rin = hist ? slot(w.H - 1) : w.r;
+        if (k == 1 && sparse_first) {
+            int32_t* cnt = reinterpret_cast<int32_t*>(w.q);
+            KZ_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * static_cast<size_t>(w.bpad) * n, st));
+            const dim3 wgrid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(64, g->max_deg))),
+                             static_cast<unsigned>(w.bpad));
+            KZ_DISPATCH_C(C, walk2_count_kernel<CC><<<wgrid, kThreads, 0, st>>>(cnt, n * CC, g->rowptr, g->colidx,
+                                                                                w.qpos, b);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            KZ_DISPATCH_C(C, cg_sparse_pq_kernel<CC><<<w.bpad, kThreads, 0, st>>>(rin, cnt, n * CC, g->rowptr,
+                                                                                  g->colidx, w.qpos, a->beta, s, k);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red,
+                                                                              FIN_CG_CONV, s, k, cnt, a->beta);
+                          ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, rin, n, n * CC, n * CC, n * CC, nb, s, k); ::kz::note_launch());
+            KZ_LAUNCH_CHECK();
+            return KZ_OK;
+        }
+        if (int rc = launch_spmm(g, C, nchunks, k1_args(w.p, nullptr, k), st)) return rc;
+        KZ_DISPATCH_C(C, cg_update_kernel<CC><<<sgrid, kThreads, 0, st>>>(rin, w.q, n, n * CC, n * CC, w.red, FIN_CG_CONV, s, k); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
-        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(xk, w.p, rcur, n, n * CC, n * CC, n * CC, nb, s, k, ah, bh, pin != w.p ? pin : nullptr); ::kz::note_launch());
+        KZ_DISPATCH_C(C, cg_pupdate_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.x, w.p, rin, n, n * CC, n * CC, n * CC, nb, s, k); ::kz::note_launch());
         KZ_LAUNCH_CHECK();
         return KZ_OK;
     };
     int64_t ran = 0;
     // small solves are launch-bound: replay one captured iteration per step
     int rc = use_graphs ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
-                        : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran);
+                        : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran, hist ? w.H : 0);
     if (rc) return rc;
 
     // the output pass forms x from the residual history unless it was folded

@@ -20,9 +20,13 @@ struct PinnedRing {
 
 // The shared iteration driver; also used by the LRC Schur solve in lrc.cu
 // through a callback that launches one iteration.
+// sync_k > 1: iteration sync_k is launched only after iteration sync_k - 1
+// has reported (no speculation there) -- for an iteration whose launch
+// itself costs block passes even when every column has already stopped
+// (the residual-history fold).
 template <class LaunchIter>
 int run_iterations(SolveState& s, int64_t max_iter, int lag, cudaStream_t st,
-                   LaunchIter&& launch_iter, int64_t* iters_run) {
+                   LaunchIter&& launch_iter, int64_t* iters_run, int64_t sync_k = 0) {
     static thread_local PinnedRing ring;
     if (!ring.slots) return fail(KZ_ECUDA, "pinned host buffer allocation failed");
     constexpr int R = PinnedRing::kRing;
@@ -39,7 +43,7 @@ int run_iterations(SolveState& s, int64_t max_iter, int lag, cudaStream_t st,
     int rc = KZ_OK;
     int64_t k = 1;
     for (; k <= max_iter; ++k) {
-        const int64_t j = k - 1 - lag;
+        const int64_t j = (k == sync_k && lag > 0) ? k - 1 : k - 1 - lag;
         if (j >= 1) {
             if (cudaEventSynchronize(ev[j % R]) != cudaSuccess) {
                 rc = fail(KZ_ECUDA, "event sync failed");

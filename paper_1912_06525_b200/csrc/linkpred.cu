@@ -73,10 +73,12 @@ __global__ void __launch_bounds__(kThreads)
         const double sp = sqrt(sp2);
         double cr = 0.0;
         if (sp > 0.0 && sr > 0.0) cr = fmin(1.0, fmax(-1.0, dot / (sr * sp)));
-        sc[c] = cr;
-        ss[c] = top_score[static_cast<size_t>(j) * s + c];
-        si[c] = c;
         corr_out[static_cast<size_t>(j) * s + c] = cr;
+        if (order_out) {  // the shared-memory sort keys exist only when ordering
+            sc[c] = cr;
+            ss[c] = top_score[static_cast<size_t>(j) * s + c];
+            si[c] = c;
+        }
     }
     if (!order_out) return;  // correlations only (the caller orders them)
     for (int c = m + threadIdx.x; c < P; c += blockDim.x) {

@@ -135,6 +135,15 @@ template <>
 __device__ __forceinline__ void ld_nc<1>(const double* p, double (&v)[1]) {
     v[0] = __ldg(p);
 }
+#ifndef KZ_K1_L2HINT
+#define KZ_K1_L2HINT 0  // experiments: per-row L2 eviction priority (1: hub last / tail first, 2: hub last / tail normal)
+#endif
+// gather with an L2 cache-policy operand (createpolicy), chosen per row
+__device__ __forceinline__ void ld_nc_hint4(const double* p, double (&v)[4], uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p), "l"(pol));
+}
 // Predicated gather: lanes with !pred issue no memory request and read 0.
 template <int VEC>
 __device__ __forceinline__ void ld_nc_pred(const double* p, double (&v)[VEC], bool pred) {
@@ -209,7 +218,8 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
                                             int stride, const double* __restrict__ Xc, int lg,
                                             int gbase, unsigned gmask,
                                             double (&acc)[Cfg<C>::VEC],
-                                            const double* __restrict__ vals = nullptr) {
+                                            const double* __restrict__ vals = nullptr,
+                                            int hub_rows = 0, uint64_t pol_hub = 0, uint64_t pol_tail = 0) {
     using K = Cfg<C>;
     // Software pipeline: the column indices of round k+1 are loaded while the
     // R gathers of round k are in flight.  Tail slots gather a clamped valid
@@ -250,6 +260,11 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
             }
 #if KZ_K1_PRED
             ld_nc_pred<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t], t < end - base);
+#elif KZ_K1_L2HINT
+            if constexpr (K::VEC == 4)
+                ld_nc_hint4(Xl + static_cast<size_t>(j) * C, v[t], j < hub_rows ? pol_hub : pol_tail);
+            else
+                ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #else
             ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #endif
@@ -310,6 +325,8 @@ struct SpmmArgs {
     int64_t ldxg, ldxs, ldz, ldy, ldd;
     const double* vals;  // weighted operator values (nullptr: binary pattern)
     double s0, s1, s2;
+    const double* s0v;   // per-column s0 (device [nchunks*C]); overrides s0 when set
+    int32_t hub_rows;    // KZ_K1_L2HINT experiments: rows [0, hub_rows) get the hub L2 policy
     double* partial;   // [nchunks][nseg][C] long-row segment sums
     int32_t* rowcnt;   // [nchunks][nlong] finished-segment counters
     double* gslot;     // [nchunks][ngroups][C] group dot partials
@@ -415,6 +432,14 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         idle_l = a.hook.mode == 1 && a.hook.n_active &&
                  *reinterpret_cast<volatile const int32_t*>(a.hook.n_active) == 0;
     const bool idle = __shfl_sync(0xffffffffu, idle_l, 0) != 0;
+    uint64_t pol_hub = 0, pol_tail = 0;
+#if KZ_K1_L2HINT
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hub));
+    if (KZ_K1_L2HINT == 1)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_tail));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_tail));
+#endif
 
     while (!idle) {
         int g = 0;
@@ -452,8 +477,14 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
             if (a.Z) {
                 double z[VEC];
                 ld_plain<VEC>(a.Z + static_cast<size_t>(chunk) * a.ldz + roff, z);
+                if (a.s0v) {
+                    const double* sv = a.s0v + chunk * C + lg * VEC;
 #pragma unroll
-                for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(a.s0, z[q]), y[q]);
+                    for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(sv[q], z[q]), y[q]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) y[q] = __dadd_rn(__dmul_rn(a.s0, z[q]), y[q]);
+                }
             }
             st_stream<VEC>(a.Y + static_cast<size_t>(chunk) * a.ldy + roff, y);
             if (a.want_dot) {
@@ -487,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
 #pragma unroll
                     for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
                     gather_rows<C, W>(a.colidx, a.rowptr[row], a.rowptr[row + 1], K::R, Xc, lg, gbase,
-                                      gmask, acc, a.vals);
+                                      gmask, acc, a.vals, a.hub_rows, pol_hub, pol_tail);
                     epilogue(row, acc);
                 }
             } else if (task.z == TASK_M) {
@@ -496,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
                 gather_rows<C, W>(a.colidx, a.rowptr[row] + gw * K::R, a.rowptr[row + 1], K::NGW * K::R,
-                                  Xc, lg, gbase, gmask, acc, a.vals);
+                                  Xc, lg, gbase, gmask, acc, a.vals, a.hub_rows, pol_hub, pol_tail);
                 warp_sum(acc);
                 if (gw == 0) epilogue(row, acc);
             } else {
@@ -509,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
                 gather_rows<C, W>(a.colidx, beg + gw * K::R, end, K::NGW * K::R, Xc, lg, gbase, gmask,
-                                  acc, a.vals);
+                                  acc, a.vals, a.hub_rows, pol_hub, pol_tail);
                 warp_sum(acc);
                 double* pbase = a.partial + static_cast<size_t>(chunk) * a.nseg * C;
                 int* cnt = a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lidx;
@@ -710,6 +741,13 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
     if (a.ldd == 0) a.ldd = g->rows * C;
     a.vals = g->vals;
     const bool w = g->vals != nullptr;
+#if KZ_K1_L2HINT
+    static const int hub_rows_env = [] {
+        const char* e = std::getenv("KZ_K1_HUBROWS");
+        return e ? std::atoi(e) : 131072;
+    }();
+    a.hub_rows = hub_rows_env;
+#endif
     cudaEvent_t tev = nullptr;
     if (k1_timing_on()) k1_timing_begin(st, &tev);
     // experiments: KZ_K1_CARVEOUT = preferred shared-memory carveout (percent)

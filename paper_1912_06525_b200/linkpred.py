@@ -62,7 +62,8 @@ def topk_device(scores, k, mask_op=None, mask_rows=None, self_ids=None):
     k = int(k)
     ids = torch.empty((b, k), dtype=torch.int64, device="cuda")
     vals = torch.empty((b, k), dtype=torch.float64, device="cuda")
-    counts = torch.zeros((b,), dtype=torch.int32, device="cuda")
+    # a single pass writes every count; several passes accumulate into zeros
+    counts = (torch.empty if k <= _TOPK_PASS else torch.zeros)((b,), dtype=torch.int32, device="cuda")
     keep = []
     margs = {}
     if mask_op is not None and mask_rows is not None:
