@@ -66,6 +66,13 @@ int kz_num_sms(void);
  * synchronises on them and returns the summed launch time and the number
  * of timed launches.  kz_k1_timing(0) stops recording and frees the events. */
 int kz_k1_timing(int enable);
+/* Checked builds (make EXTRA=-DKZ_CHECKED=1): kz_checked() is 1; every
+ * workspace slice gets a 256-byte red zone in front, and
+ * kz_checked_redzones(ws, offs, cap) returns how many red zones the calls of
+ * this thread carved in workspace `ws` since the last query (their byte
+ * offsets in offs[0..cap)), then forgets them.  Release builds: 0 / 0. */
+int kz_checked(void);
+int64_t kz_checked_redzones(const void* ws, int64_t* offs, int64_t cap);
 int kz_k1_timing_read(double* total_ms, long long* launches);
 
 /* ---- operator handles ------------------------------------------------- */

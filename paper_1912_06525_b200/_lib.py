@@ -141,6 +141,7 @@ class KzEigenDesc(ctypes.Structure):
 
 _lock = threading.Lock()
 _lib = None
+CHECKED = False  # a checked build (KZ_CHECKED) is loaded: poisoned workspaces, red-zone checks
 
 
 def load(require=True):
@@ -158,6 +159,8 @@ def load(require=True):
             return None
         lib = ctypes.CDLL(LIB_PATH)
         _declare(lib)
+        global CHECKED
+        CHECKED = bool(lib.kz_checked())
         _lib = lib
         return lib
 
@@ -169,6 +172,9 @@ def _declare(lib):
     lib.kz_version.restype = c.c_int
     lib.kz_launch_count.restype = c.c_longlong
     lib.kz_num_sms.restype = c.c_int
+    lib.kz_checked.restype = c.c_int
+    lib.kz_checked_redzones.argtypes = [c.c_void_p, c.POINTER(c.c_int64), c.c_int64]
+    lib.kz_checked_redzones.restype = c.c_int64
     lib.kz_k1_timing.argtypes = [c.c_int]
     lib.kz_k1_timing_read.argtypes = [c.POINTER(c.c_double), c.POINTER(c.c_longlong)]
     lib.kz_graph_create.argtypes = [i64, i64, i64, vp, vp, c.POINTER(vp)]
@@ -228,7 +234,10 @@ def error_from_status(code, lib=None):
 
 def check(code):
     if code != KZ_OK:
+        Workspace._tls.pending = []
         raise error_from_status(code)
+    if CHECKED:
+        Workspace.verify_redzones()
 
 
 def torch_cuda():
@@ -279,4 +288,35 @@ class Workspace:
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
             cache[slot] = buf
+        if CHECKED:
+            # poison (NaN doubles, -1 ints) and remember it for the red-zone check
+            buf.fill_(0xFF)
+            pend = getattr(cls._tls, "pending", None)
+            if pend is None:
+                pend = cls._tls.pending = []
+            pend.append(buf)
         return buf
+
+    @classmethod
+    def verify_redzones(cls):
+        """Checked builds: every red zone the library carved in the pending
+        workspaces still holds the 0xFF poison (no slice overran)."""
+        pend = getattr(cls._tls, "pending", None) or []
+        cls._tls.pending = []
+        if not pend:
+            return
+        import torch
+
+        lib = load()
+        for buf in pend:
+            cap = 1 << 16
+            offs = np.zeros(cap, dtype=np.int64)
+            k = lib.kz_checked_redzones(ctypes.c_void_p(buf.data_ptr()), offs.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cap)
+            if k == 0:
+                continue
+            o = torch.as_tensor(offs[: min(k, cap)], device=buf.device)
+            idx = (o[:, None] + torch.arange(256, device=buf.device)[None, :]).reshape(-1)
+            idx = idx[idx < buf.numel()]
+            bad = int((buf[idx] != 0xFF).sum().item())
+            if bad:
+                raise RuntimeError(f"checked build: {bad} red-zone bytes overwritten in a workspace")

@@ -447,6 +447,7 @@ constexpr int kMaxHist = 8;  // residual-history slots (cg.cu caps H at this)
 __device__ __forceinline__ double hist_value(const CgHistory& h, size_t e, int col) {
     double v = h.x0 ? h.x0[e] : 0.0;
     const int kc = h.kcol[col];
+    KZ_DCHECK(kc >= 0 && kc <= kMaxHist);
     for (int i = 0; i < kc; ++i) v = fma(h.coef[static_cast<size_t>(i) * h.bpad + col], h.slots[i * h.slot + e], v);
     return v;
 }
@@ -601,6 +602,7 @@ __global__ void store_gather_kernel(double* __restrict__ dst, const double* __re
         for (int e = threadIdx.x; e < TR * C; e += blockDim.x) {
             const int rr = e / C, c = e % C;
             const int64_t row = r0 + rr;
+            KZ_DCHECK(row >= rows || (iperm[row] >= 0 && iperm[row] < rows));
             const size_t e2 = static_cast<size_t>(chunk) * ld + static_cast<size_t>(row < rows ? iperm[row] : 0) * C + c;
             sm[rr * (C + 1) + c] = row < rows ? (hist.kcol ? hist_value(hist, e2, chunk * C + c) : src[e2]) : 0.0;
         }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <string>
 
 #include "katzb200.h"
@@ -44,7 +45,35 @@ constexpr int kWarps = kThreads / 32;
 int num_sms();
 inline int max_ctas_per_chunk() { return num_sms() * 8; }
 
-// Bump allocator over a caller-provided workspace (256-byte aligned slices).
+// ---- checked builds (make EXTRA=-DKZ_CHECKED=1; tools/checked_tier.sh) ----
+// compute-sanitizer is not available on the GPU pool, so a checked build
+// stands in for it: device bounds checks that trap (KZ_DCHECK), a bounded
+// spin-wait in K1's segment fix-up, and 256-byte red zones between every
+// workspace slice.  The Python layer fills each workspace with 0xFF before
+// the call (NaN doubles / -1 ints: reads of unwritten scratch poison the
+// result) and verifies after it that no red zone was written
+// (kz_checked_redzones, _lib.Workspace).
+#ifndef KZ_CHECKED
+#define KZ_CHECKED 0
+#endif
+#if KZ_CHECKED
+#define KZ_DCHECK(c)                                                                        \
+    do {                                                                                    \
+        if (!(c)) {                                                                         \
+            printf("KZ_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);                \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define KZ_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+constexpr size_t kRedzone = KZ_CHECKED ? 256 : 0;
+void note_redzone(const void* base, size_t off);  // checked builds: remembers a red zone of a carve
+
+// Bump allocator over a caller-provided workspace (256-byte aligned slices;
+// checked builds put a 256-byte red zone in front of every slice).
 struct Carver {
     char* base;
     size_t off = 0;
@@ -53,6 +82,10 @@ struct Carver {
     template <class T>
     T* take(size_t count) {
         off = (off + 255) & ~size_t(255);
+        if (kRedzone) {
+            if (base) note_redzone(base, off);
+            off += kRedzone;
+        }
         T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
         off += count * sizeof(T);
         return p;

@@ -23,6 +23,12 @@ void clear_error() { g_last_error.clear(); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// red zones of the workspaces carved by this thread since the last query
+static thread_local std::vector<std::pair<const void*, size_t>> g_redzones;
+void note_redzone(const void* base, size_t off) {
+    if (g_redzones.size() < (1u << 20)) g_redzones.emplace_back(base, off);
+}
+
 int num_sms() {
     static std::mutex mu;
     static std::vector<int> cache;  // per device ordinal
@@ -108,6 +114,19 @@ extern "C" int kz_k1_timing_read(double* total_ms, long long* launches) {
 }
 
 extern "C" int kz_num_sms(void) { return num_sms(); }
+
+extern "C" int kz_checked(void) { return KZ_CHECKED; }
+
+extern "C" int64_t kz_checked_redzones(const void* ws, int64_t* offs, int64_t cap) {
+    int64_t k = 0;
+    for (const auto& z : g_redzones)
+        if (z.first == ws) {
+            if (offs && k < cap) offs[k] = static_cast<int64_t>(z.second);
+            ++k;
+        }
+    g_redzones.clear();
+    return k;
+}
 
 namespace {
 

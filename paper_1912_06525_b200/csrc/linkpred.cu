@@ -26,8 +26,10 @@ __global__ void profile_gather_kernel(const double* __restrict__ S, int64_t n,
     for (int t = blockIdx.x; t < ntrip; t += gridDim.x) {
         const int64_t src = trip[3 * t], j = trip[3 * t + 1], slot = trip[3 * t + 2];
         const int m = count[j];
+        KZ_DCHECK(m >= 0 && m <= s && slot >= 0 && slot < T1);
         for (int c = threadIdx.x; c < m; c += blockDim.x) {
             const int64_t id = top[j * s + c];
+            KZ_DCHECK(id >= 0 && id < n);
             prof[(j * T1 + slot) * s + c] = S[src * n + id];
         }
     }

@@ -219,7 +219,8 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
                                             int gbase, unsigned gmask,
                                             double (&acc)[Cfg<C>::VEC],
                                             const double* __restrict__ vals = nullptr,
-                                            int hub_rows = 0, uint64_t pol_hub = 0, uint64_t pol_tail = 0) {
+                                            int hub_rows = 0, uint64_t pol_hub = 0, uint64_t pol_tail = 0,
+                                            int ncols = 0x7fffffff) {
     using K = Cfg<C>;
     // Software pipeline: the column indices of round k+1 are loaded while the
     // R gathers of round k are in flight.  Tail slots gather a clamped valid
@@ -258,6 +259,7 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
                 j = __shfl_sync(gmask, idx[t / K::G], gbase + (t % K::G));
                 if constexpr (W) w[t] = __shfl_sync(gmask, wv[t / K::G], gbase + (t % K::G));
             }
+            KZ_DCHECK(j >= 0 && j < ncols);
 #if KZ_K1_PRED
             ld_nc_pred<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t], t < end - base);
 #elif KZ_K1_L2HINT
@@ -512,13 +514,15 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         const int t_end = a.group_first[gl + 1];
         for (int t = a.group_first[gl]; t < t_end; ++t) {
             const int4 task = a.tasks[t];
+            KZ_DCHECK(task.x >= 0 && task.x < a.rows);
             if (task.z == TASK_S) {
+                KZ_DCHECK(task.y <= a.rows);
                 for (int row = task.x + gw; row < task.y; row += K::NGW) {
                     double acc[VEC];
 #pragma unroll
                     for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
                     gather_rows<C, W>(a.colidx, a.rowptr[row], a.rowptr[row + 1], K::R, Xc, lg, gbase,
-                                      gmask, acc, a.vals, a.hub_rows, pol_hub, pol_tail);
+                                      gmask, acc, a.vals, a.hub_rows, pol_hub, pol_tail, a.cols);
                     epilogue(row, acc);
                 }
             } else if (task.z == TASK_M) {
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
                 gather_rows<C, W>(a.colidx, a.rowptr[row] + gw * K::R, a.rowptr[row + 1], K::NGW * K::R,
-                                  Xc, lg, gbase, gmask, acc, a.vals, a.hub_rows, pol_hub, pol_tail);
+                                  Xc, lg, gbase, gmask, acc, a.vals, a.hub_rows, pol_hub, pol_tail, a.cols);
                 warp_sum(acc);
                 if (gw == 0) epilogue(row, acc);
             } else {
@@ -536,11 +540,12 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
                 const int s0 = a.long_seg0[lidx], nseg = a.long_seg0[lidx + 1] - s0;
                 const int2 sr = a.seg_range[s0 + k];
                 const int beg = sr.x, end = sr.y;
+                KZ_DCHECK(k < nseg && beg >= a.rowptr[row] && end <= a.rowptr[row + 1]);
                 double acc[VEC];
 #pragma unroll
                 for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
                 gather_rows<C, W>(a.colidx, beg + gw * K::R, end, K::NGW * K::R, Xc, lg, gbase, gmask,
-                                  acc, a.vals, a.hub_rows, pol_hub, pol_tail);
+                                  acc, a.vals, a.hub_rows, pol_hub, pol_tail, a.cols);
                 warp_sum(acc);
                 double* pbase = a.partial + static_cast<size_t>(chunk) * a.nseg * C;
                 int* cnt = a.rowcnt + static_cast<size_t>(chunk) * a.nlong + lidx;
@@ -555,7 +560,15 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
                     // last segment: the others were dequeued earlier by running
                     // warps; wait for them and combine in segment order
                     if (lane == 0) {
+#if KZ_CHECKED
+                        long long spins = 0;
+                        while (atomicAdd(cnt, 0) < nseg - 1) {
+                            __nanosleep(64);
+                            KZ_DCHECK(++spins < (1ll << 26));  // a lost segment would hang here
+                        }
+#else
                         while (atomicAdd(cnt, 0) < nseg - 1) __nanosleep(64);
+#endif
                         __threadfence();
                     }
                     __syncwarp();

@@ -21,13 +21,15 @@ min-degree code of libkatzb200.so.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 import scipy.sparse as sp
+from scipy.linalg import lapack
 
 from . import _lib
 from .factor import BlockCholesky, DenseCholesky, FactorizationError, LazyFactors, SpectrumError
-from .graph import InadmissibleAlphaError
+from .graph import DeviceOperator, InadmissibleAlphaError
 
 
 def build_blocks(g, alpha, bp):
@@ -127,78 +129,153 @@ def dense_cholesky(m22):
 
 
 # -- device applications ------------------------------------------------------
+# apply_correction / apply_approx_schur_inverse run on the library's own
+# kernels (kz_lrc_apply: K1 SpMMs and the DMMA L^-1 products), through a
+# kz_lrc handle built from exactly the operands the reference function
+# receives and cached per operand identity.
 _cache = {}
+_lock = threading.Lock()
 
 
-def _dev(torch, key, make):
-    """Device copy of a host operand, cached per (tag, object identity)."""
-    tag, obj = key
-    k = (tag, id(obj))
-    hit = _cache.get(k)
-    if hit is None or hit[0] is not obj:
-        hit = (obj, make())
-        _cache[k] = hit
-    return hit[1]
+def _cached(key, objs, make):
+    """make() once per (key, identity of objs); the cached value keeps the
+    objects alive so their ids stay unique."""
+    k = (key,) + tuple(id(o) for o in objs)
+    with _lock:
+        hit = _cache.get(k)
+        if hit is None or any(a is not b for a, b in zip(hit[0], objs)):
+            hit = (tuple(objs), make())
+            _cache[k] = hit
+        return hit[1]
 
 
-def _dev_factor(torch, dc):
-    return _dev(torch, ("L", dc), lambda: torch.as_tensor(np.asarray(dc.factor), dtype=torch.float64, device="cuda"))
+class _FactorHandle:
+    """A kz_lrc handle over (L, U, sigma) and optionally M12 / M11^-1: the
+    operands of apply_approx_schur_inverse (factor.py:322-337) or
+    apply_correction (factor.py:196-202).  M12 is a weighted K1 operator with
+    the caller's values (beta = -1 so the kernels' -beta*M12 x is M12 x)."""
+
+    def __init__(self, dc, lr=None, m12=None, bc=None):
+        from .lrc import _Handle, interior_inverse_csr, pad_even
+
+        torch = _lib.torch_cuda()
+        lib = _lib.load()
+        self.lib = lib
+        lf = np.asarray(dc.factor, dtype=np.float64)
+        n2 = lf.shape[0]
+        n1 = 0 if m12 is None else int(m12.shape[0])
+        ell = 0 if lr is None else int(lr.ell)
+        self.n1, self.n2, self.ell = n1, n2, ell
+        n = n1 + n2
+        empty = np.zeros(n + 1, dtype=np.int64)
+        self.full = DeviceOperator(empty, np.zeros(0, dtype=np.int32), n)
+        self.a22 = DeviceOperator(np.zeros(n2 + 1, dtype=np.int64), np.zeros(0, dtype=np.int32), n2)
+        self.a12 = self.a21 = self.minv = None
+        if n1 > 0:
+            m = sp.csr_matrix(m12)
+            m.sort_indices()
+            mt = m.T.tocsr()
+            mt.sort_indices()
+
+            def weighted(c, rows, cols):
+                h = ctypes.c_void_p()
+                o = np.ascontiguousarray(c.indptr, dtype=np.int64)
+                ci = np.ascontiguousarray(c.indices, dtype=np.int32)
+                v = np.ascontiguousarray(c.data, dtype=np.float64)
+                _lib.check(lib.kz_graph_create_weighted(rows, cols, int(o[-1]), o.ctypes.data, ci.ctypes.data,
+                                                        v.ctypes.data, ctypes.byref(h)))
+                return _Handle(lib, h)
+
+            self.a12 = weighted(m, n1, n2)
+            self.a21 = weighted(mt, n2, n1)
+
+            class _Parts:  # interior_inverse_csr reads .bc and .n1
+                pass
+
+            sh = _Parts()
+            sh.bc, sh.n1 = bc, n1
+            o, c, w = interior_inverse_csr(sh)
+            self.minv = weighted(sp.csr_matrix((w, c, o), shape=(n1, n1)), n1, n1)
+        linv, info = lapack.dtrtri(lf, lower=1)
+        if info != 0:
+            raise FactorizationError("separator factor is singular")
+        linv = np.tril(linv)
+        self.t_linv = pad_even(torch, linv)
+        self.t_linvT = pad_even(torch, linv.T)
+        self.t_u = self.t_udT = None
+        sigma = np.zeros(0)
+        if ell > 0:
+            sigma = np.ascontiguousarray(lr.values[:ell], dtype=np.float64)
+            u = np.asarray(lr.vectors, dtype=np.float64)[:, :ell]
+            with np.errstate(divide="ignore"):
+                d = 1.0 / (1.0 - sigma) - 1.0
+            self.t_u = pad_even(torch, u)
+            self.t_udT = pad_even(torch, (u * d).T)
+        self._sigma = sigma
+        desc = _lib.KzLrcDesc()
+        desc.n, desc.n1, desc.n2, desc.ell = n, n1, n2, ell
+        desc.beta = -1.0
+        desc.full = self.full.handle.value
+        desc.a12 = self.a12.handle.value if self.a12 else None
+        desc.a21 = self.a21.handle.value if self.a21 else None
+        desc.a22 = self.a22.handle.value
+        desc.minv = self.minv.handle.value if self.minv else None
+        desc.linv, desc.linvT = self.t_linv.data_ptr(), self.t_linvT.data_ptr()
+        desc.u = self.t_u.data_ptr() if self.t_u is not None else None
+        desc.udT = self.t_udT.data_ptr() if self.t_udT is not None else None
+        desc.sigma = ctypes.cast(sigma.ctypes.data, ctypes.POINTER(ctypes.c_double)) if ell > 0 else None
+        h = ctypes.c_void_p()
+        _lib.check(lib.kz_lrc_create(ctypes.byref(desc), ctypes.byref(h)))
+        self.handle = h
+
+    def apply(self, op, v):
+        torch = _lib.torch_cuda()
+        lib = self.lib
+        x = torch.as_tensor(np.asarray(v, dtype=np.float64)).cuda().reshape(1, -1).contiguous()
+        out = torch.empty((1, self.n2), dtype=torch.float64, device="cuda")
+        ws = _lib.Workspace.get(torch, lib.kz_lrc_workspace_bytes(self.handle, 1, 1), slot="lrc_apply")
+        _lib.check(lib.kz_lrc_apply(self.handle, op, 1, _lib.ptr(x), None, _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                                    _lib.stream_ptr(torch)))
+        return out[0].cpu().numpy()
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.kz_lrc_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
 
 
-def _solve_lower(torch, lf, v, transpose=False):
-    if transpose:  # L^-T v
-        return torch.linalg.solve_triangular(lf.T, v.reshape(-1, 1), upper=True).reshape(-1)
-    return torch.linalg.solve_triangular(lf, v.reshape(-1, 1), upper=False).reshape(-1)
+_KZ_LRC_PRECOND = 1
+_KZ_LRC_CORRECTION = 3
 
 
 def apply_correction(dc, m12, bc, v):
-    """R v = L^-1 M12' M11^-1 M12 L^-T v (factor.py:196-202) on the device."""
-    from .lrc import interior_inverse_csr
-
-    torch = _lib.torch_cuda()
-    lf = _dev_factor(torch, dc)
-    key12 = m12  # cache on the caller's object
-    m12 = sp.csr_matrix(m12)
-    n1 = m12.shape[0]
-    vt = torch.as_tensor(np.asarray(v, dtype=np.float64), device="cuda")
-    y = _solve_lower(torch, lf, vt, transpose=True)
-    if n1 == 0:
-        return np.zeros(np.shape(v))
-    s12 = _dev(torch, ("M12", key12), lambda: torch.sparse_csr_tensor(
-        torch.as_tensor(m12.indptr, dtype=torch.int64), torch.as_tensor(m12.indices, dtype=torch.int64),
-        torch.as_tensor(m12.data, dtype=torch.float64), size=m12.shape).cuda())
-    s21 = _dev(torch, ("M21", key12), lambda: (lambda t: torch.sparse_csr_tensor(
-        torch.as_tensor(t.indptr, dtype=torch.int64), torch.as_tensor(t.indices, dtype=torch.int64),
-        torch.as_tensor(t.data, dtype=torch.float64), size=t.shape).cuda())(m12.T.tocsr()))
-
-    class _Shim:  # interior_inverse_csr reads .bc and .n1
-        pass
-
-    def make_minv():
-        sh = _Shim()
-        sh.bc, sh.n1 = bc, n1
-        o, c, w = interior_inverse_csr(sh)
-        return torch.sparse_csr_tensor(torch.as_tensor(o, dtype=torch.int64), torch.as_tensor(c, dtype=torch.int64),
-                                       torch.as_tensor(w, dtype=torch.float64), size=(n1, n1)).cuda()
-
-    minv = _dev(torch, ("Minv", bc), make_minv)
-    w1 = s12 @ y
-    u = minv @ w1
-    z = s21 @ u
-    return _solve_lower(torch, lf, z).cpu().numpy()
+    """R v = L^-1 M12' M11^-1 M12 L^-T v (factor.py:196-202) on the device:
+    kz_lrc_apply(KZ_LRC_CORRECTION) -- K1 SpMMs with M12 / M11^-1 and the
+    DMMA L^-1 products."""
+    n2 = np.asarray(dc.factor).shape[0]
+    if np.shape(v) != (n2,):
+        raise ValueError("vector has the wrong length")
+    if n2 == 0 or sp.csr_matrix(m12).shape[0] == 0:
+        return np.zeros(n2)
+    h = _cached("corr", (dc, m12, bc), lambda: _FactorHandle(dc, m12=m12, bc=bc))
+    return h.apply(_KZ_LRC_CORRECTION, v)
 
 
 def apply_approx_schur_inverse(dc, lr, r):
-    """L^-T (I + U D U') L^-1 r, D = 1/(1 - sigma) - 1 (factor.py:322-337)."""
+    """L^-T (I + U D U') L^-1 r, D = 1/(1 - sigma) - 1 (factor.py:322-337), on
+    the device: kz_lrc_apply(KZ_LRC_PRECOND) (DMMA L^-1 products, the
+    low-rank term on the same kernels)."""
     vals = np.asarray(lr.values, dtype=np.float64)
     if np.any(vals >= 1.0):
         raise SpectrumError("correction eigenvalue at or above 1")
-    torch = _lib.torch_cuda()
-    lf = _dev_factor(torch, dc)
-    rt = torch.as_tensor(np.asarray(r, dtype=np.float64), device="cuda")
-    t = _solve_lower(torch, lf, rt)
-    if lr.ell:
-        u = _dev(torch, ("U", lr), lambda: torch.as_tensor(np.asarray(lr.vectors), dtype=torch.float64, device="cuda"))
-        d = torch.as_tensor(1.0 / (1.0 - vals) - 1.0, device="cuda")
-        t = t + u @ ((u.T @ t) * d)
-    return _solve_lower(torch, lf, t, transpose=True).cpu().numpy()
+    n2 = np.asarray(dc.factor).shape[0]
+    if np.shape(r) != (n2,):
+        raise ValueError("vector has the wrong length")
+    if n2 == 0:
+        return np.zeros(0)
+    h = _cached("precond", (dc, lr), lambda: _FactorHandle(dc, lr=lr))
+    return h.apply(_KZ_LRC_PRECOND, r)

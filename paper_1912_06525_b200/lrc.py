@@ -74,6 +74,16 @@ def interior_inverse_csr(idx):
     return offsets, cols, vals
 
 
+def pad_even(torch, a):
+    """Row-major device copy with the leading dimension rounded up to even,
+    zero padded (the kernels load entry pairs as one 16-byte access)."""
+    a = np.asarray(a, dtype=np.float64)
+    rows, cols = a.shape
+    out = np.zeros((rows, cols + (cols & 1)))
+    out[:, :cols] = a
+    return torch.as_tensor(out).cuda()
+
+
 class DeviceLRC:
     """kz_lrc handle plus the device tensors it borrows."""
 
@@ -102,13 +112,7 @@ class DeviceLRC:
                                                     v.ctypes.data, ctypes.byref(h)))
             self.minv = _Handle(lib, h)
         def dev(a):
-            # row-major with the leading dimension rounded up to even, zero
-            # padded (the kernels load entry pairs as one 16-byte access)
-            a = np.asarray(a, dtype=np.float64)
-            rows, cols = a.shape
-            out = np.zeros((rows, cols + (cols & 1)))
-            out[:, :cols] = a
-            return torch.as_tensor(out).cuda()
+            return pad_even(torch, a)
 
         self.t_linv = self.t_linvT = self.t_u = self.t_udT = None
         sigma = np.ascontiguousarray(idx.lr.values[:ell], dtype=np.float64)

@@ -448,3 +448,41 @@ def test_vec_op_rounds_like_numpy(torch, kz):
     assert np.array_equal(out.cpu().numpy(), y + b * x)
     _lib.vec_op(torch, lib, 1, n, 7.25, xt, 0.0, None, out)
     assert np.array_equal(out.cpu().numpy(), x / 7.25)
+
+
+def test_repeated_launches_are_bit_identical(torch, kz):
+    """Stand-in for racecheck (compute-sanitizer is not available on the GPU
+    pool): every kernel family with cross-warp / cross-CTA reductions or
+    spin-waits -- K1's last-finisher dot reduction and segment fix-up, the
+    CG and LRC loops, top-k, the K7 rerank -- must give bit-identical results
+    on repeated launches (any race in those protocols shows up as run-to-run
+    differences)."""
+    rec, n = chunglu_fixture()
+    g = kz.Graph(n=n, row_offsets=rec["row_offsets"], col_indices=rec["col_indices"], original_ids=np.arange(n))
+    beta = float(rec["beta"])
+    idx = kz.GraphIndex(g, beta)
+    op = idx.operator()
+    qs = rec["queries"]
+    for b, C in ((1, 1), (8, 8), (40, 32), (64, 32)):
+        X = torch.randn(b * n, dtype=torch.float64, device="cuda")
+        outs = []
+        for _ in range(4):
+            Y = torch.empty_like(X)
+            d = torch.empty(b, dtype=torch.float64, device="cuda")
+            op.spmm(X, Y, b=b, chunk=C, Xs=X, s1=1.0, s2=-beta, dots=d)
+            outs.append((Y.clone(), d.clone()))
+        for Y, d in outs[1:]:
+            assert torch.equal(Y, outs[0][0]) and torch.equal(d, outs[0][1])
+    runs = [kz.query_cg_baseline_batch(idx, qs, tol=1e-10, device=True) for _ in range(3)]
+    for s, r in runs[1:]:
+        assert torch.equal(s, runs[0][0])
+        assert [x.iterations for x in r] == [x.iterations for x in runs[0][1]]
+    kr = [[p.candidates for p in kz.katz_rank_batch(idx, qs, 30)] for _ in range(3)]
+    assert kr[0] == kr[1] == kr[2]
+    sk = [[p.candidates for p in kz.sparse_katz_batch(idx, qs[:6], 12)] for _ in range(3)]
+    assert sk[0] == sk[1] == sk[2]
+    li = kz.load_index(os.path.join(GOLDEN, "ba1200.klrc"))
+    lq = li.id_map[::97][:12]
+    lr = [kz.query_batch(li, lq, tol=1e-10) for _ in range(3)]
+    for s, r in lr[1:]:
+        assert np.array_equal(s, lr[0][0])
