@@ -238,6 +238,16 @@ int kz_pearson_rerank(const double* profiles, const double* ref, const int64_t* 
  * labels[i] = smallest node id of i's component (the order in which the
  * reference's BFS numbers components, graph.py:211-229), from device edge
  * endpoints src/dst (int32[nnz], any orientation, duplicates allowed). */
+/* from_edges (graph.py:111-148) on the device: drop self-loops, symmetrise,
+ * deduplicate, columns sorted within rows (two radix sorts of the 64-bit
+ * keys u*n+v and a unique pass) -- the reference's CSR byte for byte.
+ * u, v: device int64[m] endpoints in [0, n) (KZ_EARG otherwise).  Outputs:
+ * row_offsets device int64[n+1]; col device int32 and src device int32 (the
+ * row of each entry; may be NULL), both with capacity 2*m; *nnz_out (host)
+ * = stored entries.  Workspace: kz_edges_to_csr_workspace_bytes(n, m). */
+size_t kz_edges_to_csr_workspace_bytes(int64_t n, int64_t m);
+int kz_edges_to_csr(int64_t n, int64_t m, const int64_t* u, const int64_t* v, int64_t* row_offsets, int32_t* col,
+                    int32_t* src, int64_t* nnz_out, void* ws, size_t ws_bytes, void* stream);
 int kz_connected_components(int64_t n, int64_t nnz, const int32_t* src, const int32_t* dst,
                             int32_t* labels, void* stream);
 

@@ -197,6 +197,9 @@ def _declare(lib):
     lib.kz_pearson_rerank.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp]
     lib.kz_graph_create_weighted.argtypes = [i64, i64, i64, vp, vp, vp, c.POINTER(vp)]
     lib.kz_connected_components.argtypes = [i64, i64, vp, vp, vp, vp]
+    lib.kz_edges_to_csr_workspace_bytes.argtypes = [i64, i64]
+    lib.kz_edges_to_csr_workspace_bytes.restype = sz
+    lib.kz_edges_to_csr.argtypes = [i64, i64, vp, vp, vp, vp, vp, c.POINTER(c.c_int64), vp, sz, vp]
     lib.kz_lrc_create.argtypes = [c.POINTER(KzLrcDesc), c.POINTER(vp)]
     lib.kz_lrc_destroy.argtypes = [vp]
     lib.kz_lrc_info.argtypes = [vp, c.POINTER(i64), c.POINTER(i64), c.POINTER(i64), c.POINTER(i64)]

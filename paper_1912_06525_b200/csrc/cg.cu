@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "driver.cuh"
@@ -167,13 +168,13 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_CUDA(cudaEventRecord(e0, st));
     }
     // zero state + counters (contiguous from s.rs to the end of qpos)
-    KZ_CUDA(cudaMemsetAsync(s.rs, 0, reinterpret_cast<char*>(w.qpos) - reinterpret_cast<char*>(s.rs), st));
+    KZ_CUDA(zero_span(s.rs, w.qpos, st));
     KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nchunks, st));
     if (int rc = zero_spmm_counters(g, nchunks, w.sp, st)) return rc;
     const size_t blk_elems = static_cast<size_t>(w.bpad) * n;
     const size_t blk_bytes = sizeof(double) * blk_elems;
     const double work = static_cast<double>(g->nnz + n) * w.bpad;
-    const bool use_graphs = work <= kGraphWork && graphs_enabled();
+    const bool use_graphs = use_graph_loop(work);
     // residual-history mode (blockops.cuh CgHistory): x is formed at the end
     // from the kept residuals instead of being updated every iteration
     const bool hist = w.H >= 3 && !use_graphs;
@@ -462,9 +463,24 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         return KZ_OK;
     };
     int64_t ran = 0;
-    // small solves are launch-bound: replay one captured iteration per step
-    int rc = use_graphs ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
-                        : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran, hist ? w.H : 0);
+    long long per_iter = 0;
+    int rc;
+    if (use_graphs) {
+        // small solves are launch-bound: the whole loop is one cached graph
+        // with a device-side WHILE condition (driver.cuh)
+        GraphKey key;
+        key.v[0] = g->uid;
+        key.v[1] = reinterpret_cast<uint64_t>(ws);
+        key.v[2] = ws_bytes;
+        key.v[3] = static_cast<uint64_t>(b) | (static_cast<uint64_t>(has_x0) << 32);
+        std::memcpy(&key.v[4], &a->beta, sizeof(double));
+        std::memcpy(&key.v[5], &a->tol, sizeof(double));
+        key.v[6] = static_cast<uint64_t>(s.max_iter);
+        key.v[7] = reinterpret_cast<uint64_t>(eig);
+        rc = run_iterations_graph(s, st, launch_iter, key, &per_iter);
+    } else {
+        rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran, hist ? w.H : 0);
+    }
     if (rc) return rc;
 
     // the output pass forms x from the residual history unless it was folded
@@ -498,6 +514,11 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_CUDA(cudaEventElapsedTime(a->device_ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+    }
+    if (use_graphs) {  // loop iterations the graph ran: at least one, else the longest column
+        int64_t mx = 1;
+        for (int j = 0; j < b; ++j) mx = std::max<int64_t>(mx, iters[j]);
+        add_launches(per_iter * mx);
     }
     bool notspd = false;
     for (int j = 0; j < b; ++j) {

@@ -15,6 +15,7 @@ int fail(int code, const std::string& msg);  // records msg, returns code
 void clear_error();
 void note_launch();  // counts every kernel launch of the library (kz_launch_count)
 void add_launches(long long n);
+uint64_t next_uid();  // process-unique handle ids
 // K1 launch timing for bench.py (kz_k1_timing): when enabled, every K1
 // launch outside stream capture is bracketed by two CUDA events on its
 // own stream; kz_k1_timing_read sums their elapsed times.
@@ -71,6 +72,15 @@ inline int max_ctas_per_chunk() { return num_sms() * 8; }
 #endif
 constexpr size_t kRedzone = KZ_CHECKED ? 256 : 0;
 void note_redzone(const void* base, size_t off);  // checked builds: remembers a red zone of a carve
+void forget_redzones(const void* p0, const void* p1);  // ... and drops those inside [p0, p1)
+
+// zero the contiguous span [p0, p1) of a workspace that covers several
+// carved slices (counter / state blocks zeroed by one memset); in checked
+// builds the red zones inside the span are zeroed too, so they are dropped
+inline cudaError_t zero_span(void* p0, void* p1, cudaStream_t st) {
+    if (kRedzone) forget_redzones(p0, p1);
+    return cudaMemsetAsync(p0, 0, static_cast<size_t>(static_cast<char*>(p1) - static_cast<char*>(p0)), st);
+}
 
 // Bump allocator over a caller-provided workspace (256-byte aligned slices;
 // checked builds put a 256-byte red zone in front of every slice).

@@ -100,114 +100,126 @@ struct StreamScope {
     }
 };
 
-// solves with at most this much per-iteration work ((nnz + n) * columns)
-// replay a captured iteration graph (launch overhead dominates below it)
-constexpr double kGraphWork = 2e9;
-// Opt-in (KZ_GRAPHS=1): measured with tools/timeline.py, capture +
-// instantiate costs 0.2-1.2 ms per solve while the loop's launch gaps are
-// ~10 us per kernel, so at every BASELINE config the host-driven loop is as
-// fast or faster (R-MAT 18, 64 queries: 3.37 vs 4.55 ms span).
-inline bool graphs_enabled() {
-    static const bool on = std::getenv("KZ_GRAPHS") != nullptr;
-    return on;
+// ---- device-driven iteration loop (CUDA graph with a conditional WHILE node) ----
+// One solver iteration is captured once into the body of a WHILE node whose
+// condition a one-thread tick kernel sets from the device state (columns
+// still active, no error, iteration budget left) and which advances the
+// device iteration counter; kernels of the loop read the iteration number
+// from SolveState::iter_dev (cur_iter).  The instantiated graph is cached per
+// thread, keyed by everything the captured kernels see (operator handle id,
+// workspace, batch width, beta, tol, max_iter), so a repeated solve costs one
+// graph launch for the whole loop: no per-iteration host work or polling.
+// Used for solves whose per-iteration work is small (launch-bound: cfg1,
+// cfg2); KZ_GRAPHS=0 turns it off, KZ_GRAPHS=1 forces it on.
+constexpr double kGraphWork = 2e9;  // (nnz + n) * columns per iteration
+inline int graphs_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("KZ_GRAPHS");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;  // -1: by size
+    }();
+    return m;
+}
+inline bool use_graph_loop(double work) {
+    const int m = graphs_mode();
+    return m == 1 || (m == -1 && work <= kGraphWork);
 }
 
-struct MappedRing {
-    static constexpr int kRing = 8;
-    volatile int32_t* host = nullptr;  // [3*kRing]: n_active, err, iteration stamp
-    int32_t* dev = nullptr;
-    MappedRing() {
-        void* h = nullptr;
-        if (cudaHostAlloc(&h, sizeof(int32_t) * 3 * kRing, cudaHostAllocMapped) != cudaSuccess) return;
-        void* d = nullptr;
-        if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
-            cudaFreeHost(h);
-            return;
-        }
-        host = static_cast<volatile int32_t*>(h);
-        dev = static_cast<int32_t*>(d);
-    }
-    ~MappedRing() {
-        if (host) cudaFreeHost(const_cast<int32_t*>(host));
+struct GraphKey {
+    uint64_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool operator==(const GraphKey& o) const {
+        for (int i = 0; i < 8; ++i)
+            if (v[i] != o.v[i]) return false;
+        return true;
     }
 };
 
 static __global__ void iter_set_kernel(int32_t* iter_dev, int v) { *iter_dev = v; }
 
-static __global__ void iter_tick_kernel(SolveState s, int32_t* ring, int nring) {
-    const int k = *s.iter_dev;
-    int32_t* slot = ring + 3 * (k % nring);
-    slot[0] = *s.n_active;
-    slot[1] = *s.err;
-    __threadfence_system();
-    reinterpret_cast<volatile int32_t*>(slot)[2] = k;
+static __global__ void cond_tick_kernel(SolveState s, cudaGraphConditionalHandle h) {
+    const int k = *s.iter_dev;  // the iteration that just ran
+    const bool go = *s.n_active > 0 && *s.err == 0 && k < s.max_iter;
     *s.iter_dev = k + 1;
+    cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
+struct GraphCache {
+    static constexpr int kN = 8;
+    struct Entry {
+        GraphKey key;
+        int dev = -1;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        long long per_iter = 0;
+    } e[kN];
+    int next = 0;
+    ~GraphCache() {
+        for (auto& x : e) {
+            if (x.exec) cudaGraphExecDestroy(x.exec);
+            if (x.graph) cudaGraphDestroy(x.graph);
+        }
+    }
+};
+
+// Runs the whole loop on the device; *per_iter_out = kernels per iteration
+// (the caller adds per_iter * iterations to the launch count once it knows
+// the iterations).
 template <class LaunchIter>
-int run_iterations_graph(SolveState& s, int64_t max_iter, int lag, cudaStream_t st, LaunchIter&& launch_iter,
-                         int64_t* iters_run) {
-    static thread_local MappedRing ring;
-    if (!ring.host || !s.iter_dev) return run_iterations(s, max_iter, lag, st, launch_iter, iters_run);
-    constexpr int R = MappedRing::kRing;
-    for (int i = 0; i < 3 * R; ++i) ring.host[i] = -1;
+int run_iterations_graph(SolveState& s, cudaStream_t st, LaunchIter&& launch_iter, const GraphKey& key,
+                         long long* per_iter_out) {
+    static thread_local GraphCache cache;
+    if (!s.iter_dev) return fail(KZ_EARG, "graph loop needs the device iteration counter");
+    int dev = 0;
+    KZ_CUDA(cudaGetDevice(&dev));
+    GraphCache::Entry* hit = nullptr;
+    for (auto& x : cache.e)
+        if (x.exec && x.dev == dev && x.key == key) hit = &x;
+    if (!hit) {
+        GraphCache::Entry& x = cache.e[cache.next];
+        cache.next = (cache.next + 1) % GraphCache::kN;
+        if (x.exec) cudaGraphExecDestroy(x.exec);
+        if (x.graph) cudaGraphDestroy(x.graph);
+        x = GraphCache::Entry();
+        KZ_CUDA(cudaGraphCreate(&x.graph, 0));
+        cudaGraphConditionalHandle h;
+        KZ_CUDA(cudaGraphConditionalHandleCreate(&h, x.graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = h;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        KZ_CUDA(cudaGraphAddNode(&node, x.graph, nullptr, 0, &p));
+        cudaGraph_t body = p.conditional.phGraph_out[0];
+        KZ_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        const long long before = kz_launch_count();
+        const int rc = launch_iter(0);
+        cond_tick_kernel<<<1, 1, 0, st>>>(s, h);
+        x.per_iter = kz_launch_count() - before + 1;
+        add_launches(-(x.per_iter - 1));  // captured, not launched: counted per replay
+        const cudaError_t ce = cudaStreamEndCapture(st, &body);
+        if (rc || ce != cudaSuccess) {
+            cudaGraphDestroy(x.graph);
+            x = GraphCache::Entry();
+            cudaGetLastError();
+            return rc ? rc : fail(KZ_ECUDA, std::string("graph capture failed: ") + cudaGetErrorString(ce));
+        }
+        const cudaError_t ie = cudaGraphInstantiate(&x.exec, x.graph, 0);
+        if (ie != cudaSuccess) {
+            cudaGraphDestroy(x.graph);
+            x = GraphCache::Entry();
+            cudaGetLastError();
+            return fail(KZ_ECUDA, std::string("graph instantiate failed: ") + cudaGetErrorString(ie));
+        }
+        x.key = key;
+        x.dev = dev;
+        hit = &x;
+    }
     iter_set_kernel<<<1, 1, 0, st>>>(s.iter_dev, 1);
-    KZ_LAUNCH_CHECK();
     note_launch();
-    // capture one iteration (+ tick); kernels recorded during capture are
-    // counted per replay instead
-    const long long before = kz_launch_count();
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    KZ_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = launch_iter(0);
-    iter_tick_kernel<<<1, 1, 0, st>>>(s, ring.dev, R);
-    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
-    const long long per_iter = kz_launch_count() - before + 1;
-    add_launches(-(per_iter - 1));
-    if (rc || ce != cudaSuccess) {
-        if (graph) cudaGraphDestroy(graph);
-        cudaGetLastError();
-        return rc ? rc : fail(KZ_ECUDA, std::string("graph capture failed: ") + cudaGetErrorString(ce));
-    }
-    if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
-        cudaGraphDestroy(graph);
-        cudaGetLastError();
-        return run_iterations(s, max_iter, lag, st, launch_iter, iters_run);  // host-driven fallback
-    }
-    int64_t k = 1;
-    for (; k <= max_iter; ++k) {
-        const int64_t j = k - 1 - lag;
-        if (j >= 1) {
-            volatile int32_t* slot = ring.host + 3 * (j % R);
-            long spins = 0;
-            while (slot[2] != static_cast<int32_t>(j)) {
-                if ((++spins & 0xffff) == 0) {
-                    const cudaError_t q = cudaStreamQuery(st);
-                    if (q != cudaSuccess && q != cudaErrorNotReady) {
-                        rc = fail(KZ_ECUDA, std::string("solve stream failed: ") + cudaGetErrorString(q));
-                        break;
-                    }
-                    if (q == cudaSuccess && slot[2] != static_cast<int32_t>(j)) {
-                        rc = fail(KZ_ECUDA, "iteration stamp never arrived");
-                        break;
-                    }
-                }
-            }
-            if (rc) break;
-            if (slot[0] == 0 || slot[1] != 0) break;
-        }
-        if (cudaGraphLaunch(exec, st) != cudaSuccess) {
-            rc = fail(KZ_ECUDA, "graph launch failed");
-            break;
-        }
-        add_launches(per_iter);
-    }
-    cudaStreamSynchronize(st);
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    if (iters_run) *iters_run = k - 1;
-    return rc;
+    KZ_LAUNCH_CHECK();
+    KZ_CUDA(cudaGraphLaunch(hit->exec, st));
+    if (per_iter_out) *per_iter_out = hit->per_iter;
+    return KZ_OK;
 }
 
 }  // namespace kz

@@ -22,11 +22,23 @@ int fail(int code, const std::string& msg) {
 void clear_error() { g_last_error.clear(); }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static std::atomic<uint64_t> g_uid{0};
+uint64_t next_uid() { return ++g_uid; }
 
 // red zones of the workspaces carved by this thread since the last query
 static thread_local std::vector<std::pair<const void*, size_t>> g_redzones;
 void note_redzone(const void* base, size_t off) {
     if (g_redzones.size() < (1u << 20)) g_redzones.emplace_back(base, off);
+}
+void forget_redzones(const void* p0, const void* p1) {
+    const char* a = static_cast<const char*>(p0);
+    const char* b = static_cast<const char*>(p1);
+    g_redzones.erase(std::remove_if(g_redzones.begin(), g_redzones.end(),
+                                    [&](const std::pair<const void*, size_t>& z) {
+                                        const char* q = static_cast<const char*>(z.first) + z.second;
+                                        return q >= a && q < b;
+                                    }),
+                     g_redzones.end());
 }
 
 int num_sms() {
@@ -345,6 +357,7 @@ int create_graph(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rowptr,
         if (rp[i + 1] < rp[i]) return fail(KZ_EARG, "rowptr not monotone");
 
     auto* g = new kz_graph();
+    g->uid = next_uid();
     g->rows = rows;
     g->cols = cols;
     g->nnz = nnz;

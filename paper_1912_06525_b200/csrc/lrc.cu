@@ -21,6 +21,7 @@
 // Python loop); L^-1, (L^-1)^T, U and (U D)^T are dense row-major K3/K6
 // operands.  All device memory of the handle is borrowed from the caller.
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <vector>
 
@@ -45,6 +46,7 @@ struct kz_lrc {
     // every sigma < 1: the preconditioner exists (factor.py:329-330); only
     // the calls that apply it (query, lrc_pcg, PRECOND) raise otherwise
     bool spectrum_ok = true;
+    uint64_t uid = 0;  // process-unique id (keys cached solve graphs)
 };
 
 namespace {
@@ -278,6 +280,7 @@ extern "C" int kz_lrc_create(const kz_lrc_desc* d, kz_lrc** out) {
         if (!(d->sigma[i] < 1.0)) spectrum_ok = false;
     auto* h = new kz_lrc();
     h->spectrum_ok = spectrum_ok;
+    h->uid = next_uid();
     h->n = d->n;
     h->n1 = d->n1;
     h->n2 = d->n2;
@@ -356,12 +359,13 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
         KZ_CUDA(cudaEventCreate(&e1));
         KZ_CUDA(cudaEventRecord(e0, st));
     }
-    KZ_CUDA(cudaMemsetAsync(s.rs, 0, reinterpret_cast<char*>(w.qpos) - reinterpret_cast<char*>(s.rs), st));
+    KZ_CUDA(zero_span(s.rs, w.qpos, st));
     KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nch, st));
     KZ_CUDA(cudaMemsetAsync(w.ds.cnt, 0, sizeof(int32_t) * w.ds.cnt_cap, st));
     if (int rc = zero_spmm_counters(w.dims, nch, w.sp, st)) return rc;
     const unsigned tg = static_cast<unsigned>(std::min<int64_t>(2 * max_ctas_per_chunk(), ((n + 63) / 64) * nch));
     int rc = KZ_OK;
+    long long graph_per_iter = 0;  // kernels per iteration of a graph-run loop (launch count)
 
     if (!mode_pcg) {
         KZ_CUDA(cudaMemsetAsync(w.rhs, 0, sizeof(double) * w.bpad * n, st));
@@ -452,11 +456,21 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
             return KZ_OK;
         };
         int64_t ran = 0;
-        // launch-bound small solves replay one captured PCG iteration per step
-        if ((rc = work * w.bpad <= kGraphWork && graphs_enabled()
-                      ? run_iterations_graph(s, s.max_iter, lag, st, launch_iter, &ran)
-                      : run_iterations(s, s.max_iter, lag, st, launch_iter, &ran)))
+        // launch-bound small solves: the whole PCG loop is one cached graph
+        // with a device-side WHILE condition (driver.cuh)
+        if (use_graph_loop(work * w.bpad)) {
+            GraphKey key;
+            key.v[0] = h->uid;
+            key.v[1] = reinterpret_cast<uint64_t>(ws);
+            key.v[2] = ws_bytes;
+            key.v[3] = static_cast<uint64_t>(b) | (static_cast<uint64_t>(C) << 32);
+            key.v[4] = static_cast<uint64_t>(mode_pcg) | (static_cast<uint64_t>(a->x0 != nullptr) << 1);
+            std::memcpy(&key.v[5], &a->tol, sizeof(double));
+            key.v[6] = static_cast<uint64_t>(s.max_iter);
+            if ((rc = run_iterations_graph(s, st, launch_iter, key, &graph_per_iter))) return rc;
+        } else if ((rc = run_iterations(s, s.max_iter, lag, st, launch_iter, &ran))) {
             return rc;
+        }
     }
 
     if (!mode_pcg) {
@@ -513,6 +527,11 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
         KZ_CUDA(cudaEventElapsedTime(a->device_ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+    }
+    if (graph_per_iter) {
+        int64_t mx = 1;
+        for (int j = 0; j < b; ++j) mx = std::max<int64_t>(mx, iters[j]);
+        add_launches(graph_per_iter * mx);
     }
     bool notspd = false;
     for (int j = 0; j < b; ++j) {

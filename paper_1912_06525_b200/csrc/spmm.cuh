@@ -83,6 +83,7 @@ struct kz_graph {
     int2* seg_range = nullptr;      // [nseg] CSR position range [x, y) of each segment
     int32_t nblocks = 1;            // column blocks of the long-row phases (1: unblocked)
     int32_t max_deg = 0;
+    uint64_t uid = 0;               // process-unique id (keys cached solve graphs)
 };
 
 namespace kz {
@@ -697,7 +698,7 @@ inline void carve_spmm_scratch(Carver& cv, const kz_graph* g, int nchunks, int C
 inline int zero_spmm_counters(const SpmmDims& d, int nchunks, const SpmmScratch& s, cudaStream_t st) {
     const char* b0 = reinterpret_cast<const char*>(s.rowcnt);
     const char* b1 = reinterpret_cast<const char*>(s.queue + 2);
-    KZ_CUDA(cudaMemsetAsync(s.rowcnt, 0, static_cast<size_t>(b1 - b0), st));
+    KZ_CUDA(zero_span(const_cast<char*>(b0), const_cast<char*>(b1), st));
     (void)d;
     (void)nchunks;
     return KZ_OK;

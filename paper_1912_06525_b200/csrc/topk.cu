@@ -302,6 +302,161 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) count_out[j] = take;
 }
 
+// ---- small columns: the whole select in one CTA per column -------------------
+// For n <= kSmallN the 8 radix rounds, the mask subtraction, the collect and
+// the sort run inside one CTA per column (histogram and candidates in shared
+// memory): 1 launch instead of ~27 (latency-bound configs such as cfg1).
+// Same keys, same digits, same tie order as the multi-CTA path.
+constexpr int64_t kSmallN = 65536;
+constexpr int kSmallThreads = 512;
+
+__global__ void __launch_bounds__(kSmallThreads)
+    topk_small_kernel(const double* __restrict__ scores, int64_t n, int k, MaskRef m,
+                      int64_t* __restrict__ ids_out, double* __restrict__ vals_out, int32_t* __restrict__ count_out) {
+    extern __shared__ unsigned char tsm[];
+    unsigned int* h = reinterpret_cast<unsigned int*>(tsm);                        // [kBins]
+    unsigned long long* sk = reinterpret_cast<unsigned long long*>(h + kBins);     // [kCap]
+    int* si = reinterpret_cast<int*>(sk + kCap);                                   // [kCap]
+    __shared__ ColState c;
+    __shared__ unsigned int part[kSmallThreads];
+    __shared__ int s_bin, s_cum;
+    const int j = blockIdx.x;
+    const double* col = scores + static_cast<size_t>(j) * n;
+    if (threadIdx.x == 0) {
+        c = ColState{};
+        c.shift = 96;
+        c.need = static_cast<int>(k < n ? static_cast<int64_t>(k) : n);
+    }
+    __syncthreads();
+    for (int round = 0; round < kRounds && !c.done; ++round) {
+        for (int i = threadIdx.x; i < kBins; i += kSmallThreads) h[i] = 0;
+        __syncthreads();
+        const ColState cc = c;
+        const int ns = max(cc.shift - kDigit, 0);
+        for (int64_t i = threadIdx.x; i < n; i += kSmallThreads) {
+            const unsigned long long hi = score_key(col[i]);
+            const unsigned int lo = ~static_cast<unsigned int>(i);
+            if (cmp_prefix(hi, lo, cc, cc.shift) == 0 && !above_bound(m, j, hi, lo))
+                atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
+        }
+        __syncthreads();
+        // masked ids leave the histogram (topk_mask_kernel)
+        auto visit = [&](int64_t id) {
+            const unsigned long long hi = score_key(col[id]);
+            const unsigned int lo = ~static_cast<unsigned int>(id);
+            if (cmp_prefix(hi, lo, cc, cc.shift) == 0 && !above_bound(m, j, hi, lo)) atomicSub(&h[digit_of(hi, lo, ns)], 1u);
+        };
+        const int64_t self = m.self ? m.self[j] : -1;
+        if (threadIdx.x == 0 && self >= 0) visit(self);
+        if (m.rowptr && m.rows && m.rows[j] >= 0) {
+            const int64_t r = m.rows[j];
+            for (int e = m.rowptr[r] + threadIdx.x; e < m.rowptr[r + 1]; e += kSmallThreads) {
+                const int64_t id = m.colidx[e];
+                if (id != self) visit(id);
+            }
+        }
+        __syncthreads();
+        // pivot digit (topk_select_kernel)
+        constexpr int PB = kBins / kSmallThreads;
+        unsigned int loc = 0;
+        for (int i = 0; i < PB; ++i) loc += h[threadIdx.x * PB + i];
+        part[threadIdx.x] = loc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned int cum = 0;
+            int bin = -1;
+            for (int t = kSmallThreads - 1; t >= 0 && bin < 0; --t) {
+                if (cum + part[t] >= static_cast<unsigned int>(c.need)) {
+                    for (int i = PB - 1; i >= 0; --i) {
+                        const unsigned int hv = h[t * PB + i];
+                        if (cum + hv >= static_cast<unsigned int>(c.need)) {
+                            bin = t * PB + i;
+                            break;
+                        }
+                        cum += hv;
+                    }
+                } else {
+                    cum += part[t];
+                }
+            }
+            s_bin = bin;
+            s_cum = static_cast<int>(cum);
+            if (bin < 0) {
+                c.done = 1;
+            } else {
+                const unsigned int pivot = h[bin];
+                c.above += s_cum;
+                c.need -= s_cum;
+                if (ns >= 32) {
+                    c.phi |= static_cast<unsigned long long>(bin) << (ns - 32);
+                } else {
+                    const unsigned long long v = static_cast<unsigned long long>(bin) << ns;
+                    c.plo |= static_cast<unsigned int>(v & 0xffffffffull);
+                    c.phi |= v >> 32;
+                }
+                c.shift = ns;
+                if (c.above + static_cast<int>(pivot) <= kCap || ns == 0) c.done = 1;
+            }
+        }
+        __syncthreads();
+    }
+    // collect every unmasked element at or above the pivot range
+    if (threadIdx.x == 0) c.ncand = 0;
+    __syncthreads();
+    const ColState cc = c;
+    for (int64_t i = threadIdx.x; i < n; i += kSmallThreads) {
+        const unsigned long long hi = score_key(col[i]);
+        const unsigned int lo = ~static_cast<unsigned int>(i);
+        if (cmp_prefix(hi, lo, cc, cc.shift) >= 0 && !above_bound(m, j, hi, lo) && !is_masked(m, j, i)) {
+            const int pos = atomicAdd(&c.ncand, 1);
+            if (pos < kCap) {
+                sk[pos] = hi;
+                si[pos] = static_cast<int>(i);
+            }
+        }
+    }
+    __syncthreads();
+    const int mm = min(c.ncand, kCap);
+    int P = 1;
+    while (P < mm) P <<= 1;
+    for (int i = mm + threadIdx.x; i < P; i += kSmallThreads) {
+        sk[i] = 0ull;
+        si[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    auto before = [&](int a, int b2) { return sk[a] > sk[b2] || (sk[a] == sk[b2] && si[a] < si[b2]); };
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P; i += kSmallThreads) {
+                const int partner = i ^ stride;
+                if (partner > i) {
+                    const bool desc = (i & size) == 0;
+                    const bool swap = desc ? before(partner, i) : before(i, partner);
+                    if (swap) {
+                        const unsigned long long tk = sk[i];
+                        sk[i] = sk[partner];
+                        sk[partner] = tk;
+                        const int ti = si[i];
+                        si[i] = si[partner];
+                        si[partner] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const int take = min(k, mm);
+    for (int i = threadIdx.x; i < take; i += kSmallThreads) {
+        ids_out[static_cast<size_t>(j) * k + i] = si[i];
+        vals_out[static_cast<size_t>(j) * k + i] = __longlong_as_double(static_cast<long long>(sk[i]));
+    }
+    for (int i = take + threadIdx.x; i < k; i += kSmallThreads) {
+        ids_out[static_cast<size_t>(j) * k + i] = -1;
+        vals_out[static_cast<size_t>(j) * k + i] = 0.0;
+    }
+    if (threadIdx.x == 0) count_out[j] = take;
+}
+
 struct TopkWork {
     ColState* cs;
     unsigned int* hist;
@@ -360,6 +515,20 @@ extern "C" int kz_topk_batch(const kz_topk_args* a, void* ws, size_t ws_bytes, v
     }
     m.bval = a->bound_vals;
     m.bid = a->bound_ids;
+    if (a->n <= kSmallN) {
+        constexpr size_t smem = sizeof(unsigned int) * kBins + (sizeof(unsigned long long) + sizeof(int)) * kCap;
+        static bool attr = false;
+        if (!attr) {
+            KZ_CUDA(cudaFuncSetAttribute(topk_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            attr = true;
+        }
+        topk_small_kernel<<<b, kSmallThreads, smem, st>>>(a->scores, a->n, a->k, m, a->ids_out, a->vals_out,
+                                                         a->count_out);
+        ::kz::note_launch();
+        KZ_LAUNCH_CHECK();
+        return KZ_OK;
+    }
     KZ_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(unsigned int) * b * kBins, st));
     topk_init_kernel<<<(b + 127) / 128, 128, 0, st>>>(w.cs, b, a->n, a->k); ::kz::note_launch();
     KZ_LAUNCH_CHECK();

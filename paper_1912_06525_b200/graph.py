@@ -213,31 +213,32 @@ def load_edge_list(source, fmt="auto"):
 
 
 def from_edges_device(u, v, n, original_ids=None):
-    """from_edges (graph.py:111-148) on the GPU: the same CSR (symmetric,
-    deduplicated, loop-free, columns sorted within rows).  u, v: int64
-    endpoint arrays (numpy or torch).  Returns a host Graph plus the device
-    CSR (offsets int64, columns int64) for chaining."""
+    """from_edges (graph.py:111-148) on the GPU through kz_edges_to_csr (radix
+    sort of the undirected keys, unique, directed expansion, second sort):
+    the same CSR (symmetric, deduplicated, loop-free, columns sorted within
+    rows).  u, v: int64 endpoint arrays (numpy or torch).  Returns a host
+    Graph plus the device CSR (offsets int64, columns int32, rows int32) for
+    chaining."""
     torch = _lib.torch_cuda()
-    ut = torch.as_tensor(u, dtype=torch.int64).cuda()
-    vt = torch.as_tensor(v, dtype=torch.int64).cuda()
-    keep = ut != vt
-    lo = torch.minimum(ut, vt)[keep]
-    hi = torch.maximum(ut, vt)[keep]
-    del ut, vt, keep
-    und = torch.unique(lo * n + hi)
-    del lo, hi
-    lo, hi = und // n, und % n
-    del und
-    keys, _ = torch.sort(torch.cat([lo * n + hi, hi * n + lo]))
-    del lo, hi
-    src = keys // n
-    dst = keys % n
-    del keys
-    off = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
-    off[1:] = torch.cumsum(torch.bincount(src, minlength=n), 0)
+    lib = _lib.load()
+    ut = torch.as_tensor(u, dtype=torch.int64).cuda().contiguous()
+    vt = torch.as_tensor(v, dtype=torch.int64).cuda().contiguous()
+    m = int(ut.numel())
+    if int(vt.numel()) != m:
+        raise ValueError("endpoint arrays differ in length")
+    off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    cap = max(2 * m, 1)
+    dst = torch.empty(cap, dtype=torch.int32, device="cuda")
+    src = torch.empty(cap, dtype=torch.int32, device="cuda")
+    nnz = ctypes.c_int64(0)
+    ws = torch.empty(max(int(lib.kz_edges_to_csr_workspace_bytes(n, m)), 256), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.kz_edges_to_csr(n, m, _lib.ptr(ut), _lib.ptr(vt), _lib.ptr(off), _lib.ptr(dst), _lib.ptr(src),
+                                   ctypes.byref(nnz), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(torch)))
+    del ws, ut, vt
+    dst, src = dst[: nnz.value], src[: nnz.value]
     if original_ids is None:
         original_ids = np.arange(n, dtype=np.int64)
-    g = Graph(n=n, row_offsets=off.cpu().numpy(), col_indices=dst.cpu().numpy(),
+    g = Graph(n=n, row_offsets=off.cpu().numpy(), col_indices=dst.cpu().numpy().astype(np.int64),
               original_ids=np.asarray(original_ids, dtype=np.int64))
     return g, (off, dst, src)
 
@@ -251,16 +252,15 @@ def largest_connected_component_device(g, dev=None):
     n = g.n
     if dev is None:
         off = torch.as_tensor(g.row_offsets, dtype=torch.int64).cuda()
-        dst = torch.as_tensor(g.col_indices, dtype=torch.int64).cuda()
-        src = torch.repeat_interleave(torch.arange(n, device="cuda"), off[1:] - off[:-1])
+        dst = torch.as_tensor(g.col_indices, dtype=torch.int32).cuda()
+        src = torch.repeat_interleave(torch.arange(n, device="cuda", dtype=torch.int32), off[1:] - off[:-1])
     else:
         off, dst, src = dev
     labels = torch.empty(n, dtype=torch.int32, device="cuda")
-    s32 = src.to(torch.int32)
-    d32 = dst.to(torch.int32)
+    s32 = src.to(torch.int32).contiguous()
+    d32 = dst.to(torch.int32).contiguous()
     _lib.check(lib.kz_connected_components(n, int(d32.numel()), _lib.ptr(s32), _lib.ptr(d32), _lib.ptr(labels),
                                            _lib.stream_ptr(torch)))
-    del s32, d32
     lab = labels.to(torch.int64)
     sizes = torch.bincount(lab, minlength=n)
     big = int(sizes.max().item())
@@ -271,8 +271,8 @@ def largest_connected_component_device(g, dev=None):
     keep = torch.nonzero(lab == best).flatten()
     remap = torch.full((n,), -1, dtype=torch.int64, device="cuda")
     remap[keep] = torch.arange(keep.numel(), device="cuda")
-    mask = lab[src] == best
-    cols = remap[dst[mask]]
+    mask = lab[src.long()] == best
+    cols = remap[dst[mask].long()]
     deg = (off[1:] - off[:-1])[keep]
     new_off = torch.zeros(keep.numel() + 1, dtype=torch.int64, device="cuda")
     new_off[1:] = torch.cumsum(deg, 0)

@@ -283,9 +283,10 @@ def test_cg_residual_history_matches_per_iteration_update(torch, kz, monkeypatch
         assert np.all(diff <= 1e-13), diff.max()
 
 
-def test_topk_matches_lexsort(torch, kz):
+@pytest.mark.parametrize("n", [50_000, 70_000])  # one-CTA-per-column path (n <= 65,536) and the sliced path
+def test_topk_matches_lexsort(torch, kz, n):
     rng = np.random.default_rng(4)
-    b, n = 7, 50_000
+    b = 7
     S = np.abs(rng.standard_normal((b, n)))
     S[:, ::7] = np.round(S[:, ::7], 1)  # many exact ties
     S[1, :] = 0.25  # all tied
@@ -343,9 +344,12 @@ def test_operator_rejects_out_of_range_columns(torch, kz):
         kz.DeviceOperator(off, np.array([1, -1], dtype=np.int32), 2)
 
 
-def test_graph_replayed_loops_match(kz):
-    """The opt-in CUDA-graph iteration loop (KZ_GRAPHS=1, driver.cuh) gives
-    the same CG and LRC answers as the host-driven loop."""
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_graph_replayed_loops_match(kz, mode):
+    """Both iteration drivers (driver.cuh) give the reference's CG and LRC
+    answers: the device-driven graph loop (conditional WHILE node, the
+    default for small solves; KZ_GRAPHS=1 forces it) and the host-driven
+    loop (KZ_GRAPHS=0), each run twice to exercise the cached graph."""
     import subprocess
     import sys
 
@@ -356,7 +360,7 @@ import paper_1912_06525_b200 as kz
 idx = kz.load_index("tests/golden/ba300.klrc")
 rec = np.load("tests/golden/ba300.npz")
 q = rec["queries"]
-for fn, key in ((kz.query_cg_baseline_batch, "cg"), (kz.query_batch, "lrc")):
+for fn, key in ((kz.query_cg_baseline_batch, "cg"), (kz.query_batch, "lrc")) * 2:
     s, r = fn(idx, q, tol=1e-10)
     for j in range(len(q)):
         want = rec[f"{key}_1e-10_scores"][j]
@@ -365,18 +369,19 @@ for fn, key in ((kz.query_cg_baseline_batch, "cg"), (kz.query_batch, "lrc")):
 print("graphs ok")
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, KZ_GRAPHS="1")
+    env = dict(os.environ, KZ_GRAPHS=mode)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "graphs ok" in out.stdout, out.stderr[-2000:]
 
 
-def test_topk_above_one_pass_matches_lexsort(torch, kz):
+@pytest.mark.parametrize("n", [20_000, 70_000])
+def test_topk_above_one_pass_matches_lexsort(torch, kz, n):
     """k beyond one kz_topk_batch pass (4,096 per column): the continuation
     passes (bound_vals / bound_ids) give exactly np.lexsort's order,
     including heavy ties across pass boundaries and columns with fewer
     unmasked entries than k."""
     rng = np.random.default_rng(9)
-    b, n = 3, 20_000
+    b = 3
     S = np.abs(rng.standard_normal((b, n)))
     S[0, ::3] = 0.5  # ties that straddle the 4,096 boundaries
     S[2, : n - 5000] = 0.0  # long run of equal zeros
@@ -463,7 +468,7 @@ def test_repeated_launches_are_bit_identical(torch, kz):
     idx = kz.GraphIndex(g, beta)
     op = idx.operator()
     qs = rec["queries"]
-    for b, C in ((1, 1), (8, 8), (40, 32), (64, 32)):
+    for b, C in ((1, 1), (8, 8), (40, 8), (64, 32)):
         X = torch.randn(b * n, dtype=torch.float64, device="cuda")
         outs = []
         for _ in range(4):

@@ -1,7 +1,8 @@
 """Graph ingestion against the reference's own outputs (tests/golden/ingest.npz,
 made by tests/golden/make_ingest_golden.py from lrckatz.from_edges /
 largest_connected_component / spectral_norm): the numpy restatement on CPU,
-the device path (kz_connected_components + torch sort/unique) on the GPU."""
+the device path (kz_edges_to_csr radix sort/unique + kz_connected_components)
+on the GPU."""
 
 import os
 
@@ -57,3 +58,51 @@ def test_device_rmat_matches_host_rmat():
     a, b = rmat_graph(14, seed=2), rmat_graph_fast(14, seed=2)
     assert a.n == b.n and np.array_equal(a.row_offsets, b.row_offsets)
     assert np.array_equal(a.col_indices, b.col_indices) and np.array_equal(a.original_ids, b.original_ids)
+
+
+@pytest.mark.gpu
+def test_device_from_edges_edge_cases():
+    """Duplicates in both orientations, self-loops only, no edges, isolated
+    trailing nodes, out-of-range endpoints (from_edges, graph.py:111-148)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1912_06525_b200.graph import from_edges_device
+
+    cases = [
+        (np.array([[0, 1], [1, 0], [1, 0], [2, 2], [3, 1]]), 6),
+        (np.array([[2, 2], [0, 0]]), 3),
+        (np.zeros((0, 2), dtype=np.int64), 4),
+        (np.array([[0, 4]]), 5),
+    ]
+    for e, n in cases:
+        g, _ = from_edges_device(e[:, 0], e[:, 1], n)
+        keep = e[:, 0] != e[:, 1]
+        want = kz.from_edges(e, n=n) if keep.any() else None
+        if want is None:
+            assert g.nnz == 0 and np.array_equal(g.row_offsets, np.zeros(n + 1, dtype=np.int64))
+        else:
+            assert np.array_equal(g.row_offsets, want.row_offsets)
+            assert np.array_equal(g.col_indices, want.col_indices)
+    with pytest.raises(ValueError):
+        from_edges_device(np.array([0, 5]), np.array([1, 1]), 5)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_device_ingestion_matches_oracle_at_rmat18():
+    """The BASELINE cfg2 graph (R-MAT 18) from device ingestion equals the
+    oracle's numpy/scipy restatement of from_edges + the largest component
+    byte for byte."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import katz_oracle as O
+    from paper_1912_06525_b200.generators import rmat_graph_fast
+
+    g = rmat_graph_fast(18)
+    off, col, ids = O.config_csr("cfg2")
+    assert np.array_equal(g.row_offsets, off) and np.array_equal(g.col_indices, col)
+    assert np.array_equal(g.original_ids, ids)
