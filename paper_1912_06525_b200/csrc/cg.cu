@@ -40,6 +40,7 @@
 #include <cstring>
 #include <vector>
 
+#include "cgsmall.cuh"
 #include "driver.cuh"
 #include "lowrank.cuh"
 
@@ -59,6 +60,7 @@ struct CgWork {
     int64_t* qpos;
     int64_t* iperm;  // inverse output permutation (gather-based store)
     double* y;       // eigen start: [nch][ldr][C] Galerkin coefficients
+    double* small_part;  // fused small loop (cgsmall.cuh): [2][SMs][bpad] CTA partials
 };
 
 void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* eig = nullptr) {
@@ -114,6 +116,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.qpos = cv.take<int64_t>(w.bpad);
     w.iperm = cv.take<int64_t>(g->rows);
     w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
+    w.small_part = cv.take<double>(2 * static_cast<size_t>(num_sms()) * w.bpad);
 }
 
 
@@ -174,10 +177,21 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     const size_t blk_elems = static_cast<size_t>(w.bpad) * n;
     const size_t blk_bytes = sizeof(double) * blk_elems;
     const double work = static_cast<double>(g->nnz + n) * w.bpad;
-    const bool use_graphs = use_graph_loop(work);
+    // small solves (blocks of at most kSmallCgElems doubles, <= 256 columns):
+    // the whole loop is one cooperative kernel (cgsmall.cuh); KZ_CG_FUSED=0
+    // turns it off
+    int small_grid = 0;
+    {
+        const char* fe = std::getenv("KZ_CG_FUSED");
+        if (!(fe && fe[0] == '0') && blk_elems <= kSmallCgElems && C <= 32) {
+            KZ_DISPATCH_C(C, small_grid = small_cg_grid(n, CC, w.bpad, reinterpret_cast<const void*>(cg_small_kernel<CC>)));
+        }
+    }
+    const bool fused = small_grid > 0;
+    const bool use_graphs = !fused && use_graph_loop(work);
     // residual-history mode (blockops.cuh CgHistory): x is formed at the end
     // from the kept residuals instead of being updated every iteration
-    const bool hist = w.H >= 3 && !use_graphs;
+    const bool hist = w.H >= 3 && !use_graphs && !fused;
     const bool has_x0 = eig != nullptr || a->x0 != nullptr;
     if (hist) {
         KZ_CUDA(cudaMemsetAsync(w.ahist, 0, sizeof(double) * static_cast<size_t>(w.H) * w.bpad, st));
@@ -354,7 +368,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     // turns it off
     const char* sf_env = std::getenv("KZ_CG_SPARSE_FIRST");
     const bool sparse_first_on = !(sf_env && sf_env[0] == '0');
-    const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs &&
+    const bool sparse_first = sparse_first_on && !eig && !a->rhs && !a->x0 && a->qpos && !use_graphs && !fused &&
                               w.bpad <= 65535;  // one grid row per column in walk2_count_kernel
     auto k1_args = [&](const double* xin, const double* z, int k) {
         SpmmArgs sa = make_spmm_args(g, w.sp);
@@ -465,13 +479,34 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     int64_t ran = 0;
     long long per_iter = 0;
     int rc;
-    if (use_graphs) {
+    if (fused) {
+        SmallCgArgs sa;
+        sa.rows = static_cast<int32_t>(n);
+        sa.nchunks = nchunks;
+        sa.b = b;
+        sa.bpad = w.bpad;
+        sa.rowptr = g->rowptr;
+        sa.colidx = g->colidx;
+        sa.beta = a->beta;
+        sa.x = w.x;
+        sa.r = w.r;
+        sa.p = w.p;
+        sa.q = w.q;
+        sa.part = w.small_part;
+        sa.s = s;
+        void* kargs[] = {&sa};
+        KZ_DISPATCH_C(C, KZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(cg_small_kernel<CC>),
+                                                            dim3(small_grid), dim3(kSmallCgThreads), kargs, 0, st)));
+        note_launch();
+        rc = KZ_OK;
+    } else if (use_graphs) {
         // small solves are launch-bound: the whole loop is one cached graph
         // with a device-side WHILE condition (driver.cuh)
         GraphKey key;
         key.v[0] = g->uid;
         key.v[1] = reinterpret_cast<uint64_t>(ws);
-        key.v[2] = ws_bytes;
+        // the workspace layout: history slots and eig change every offset
+        key.v[2] = static_cast<uint64_t>(w.H) | (reinterpret_cast<uint64_t>(w.q) << 8);
         key.v[3] = static_cast<uint64_t>(b) | (static_cast<uint64_t>(has_x0) << 32);
         std::memcpy(&key.v[4], &a->beta, sizeof(double));
         std::memcpy(&key.v[5], &a->tol, sizeof(double));
