@@ -60,7 +60,8 @@ struct CgWork {
     int64_t* qpos;
     int64_t* iperm;  // inverse output permutation (gather-based store)
     double* y;       // eigen start: [nch][ldr][C] Galerkin coefficients
-    double* small_part;  // fused small loop (cgsmall.cuh): [2][SMs][bpad] CTA partials
+    double* small_part;   // fused small loop (cgsmall.cuh): [2][SMs][bpad] CTA partials
+    double* small_carry;  // ... and [2][SMs * 8 warps][bpad] split-row partials
 };
 
 void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* eig = nullptr) {
@@ -117,6 +118,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.iperm = cv.take<int64_t>(g->rows);
     w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
     w.small_part = cv.take<double>(2 * static_cast<size_t>(num_sms()) * w.bpad);
+    w.small_carry = cv.take<double>(2 * static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
 }
 
 
@@ -184,7 +186,8 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     {
         const char* fe = std::getenv("KZ_CG_FUSED");
         if (!(fe && fe[0] == '0') && blk_elems <= kSmallCgElems && C <= 32) {
-            KZ_DISPATCH_C(C, small_grid = small_cg_grid(n, CC, w.bpad, reinterpret_cast<const void*>(cg_small_kernel<CC>)));
+            KZ_DISPATCH_C(C, small_grid = small_cg_grid(n, g->nnz, CC, w.bpad,
+                                                        reinterpret_cast<const void*>(cg_small_kernel<CC>)));
         }
     }
     const bool fused = small_grid > 0;
@@ -493,6 +496,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         sa.p = w.p;
         sa.q = w.q;
         sa.part = w.small_part;
+        sa.carry = w.small_carry;
         sa.s = s;
         void* kargs[] = {&sa};
         KZ_DISPATCH_C(C, KZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(cg_small_kernel<CC>),

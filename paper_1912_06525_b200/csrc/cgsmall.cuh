@@ -1,21 +1,23 @@
 // cgsmall.cuh -- the whole CG loop of a small batched solve in ONE
-// cooperative kernel (cfg1-sized problems: the vector blocks sit in L2 and
-// every separate kernel of the host- or graph-driven loop costs more in
-// launch + tail latency than in work).
+// cooperative kernel.  At cfg1 sizes (n ~ 10^4, 16 columns) the vector blocks
+// sit in L2 and every kernel of the host- or graph-driven loop costs more in
+// launch, tail and cross-CTA-reduction latency than in work; here an
+// iteration is four short phases separated by grid barriers.
 //
-// Per iteration, three phases separated by grid-wide barriers, exactly the
-// reference recurrence of cg() (solver.py:78-95) per column:
-//   1  q = p - beta*A p (gather), partial p.q per warp -> per CTA
-//   2  every CTA reduces the CTA partials of p.q in a fixed order, a = rs/pq
-//      (non-positive curvature: the column errs, the solve stops), then
-//      r -= a*q over its share with partial r.r
-//   3  every CTA reduces r.r, applies the stop test / iteration budget and
-//      b = rs'/rs, then x += a*p, p = r + b*p over its share
-// Every CTA derives the same per-column scalars from the same partials in the
-// same order, so no broadcast step is needed and results are run-to-run
-// deterministic.  CTA 0 publishes the per-column state for the reports.
-// Rows are cut into cost-balanced contiguous warp segments (cost = entries +
-// rows, a binary search of rowptr), fixed for the whole solve.
+// Per iteration, exactly the reference recurrence of cg() (solver.py:78-95)
+// for every column:
+//   1  q = p - beta*A p over a merge-path share of (rows + entries) per warp,
+//      8 gathers in flight per lane; a row split across warps leaves carries
+//   2  the warp that owns a split row's end adds the carries (warp order) and
+//      finishes it; p.q partials per CTA
+//   3  every CTA reduces the CTA partials in a fixed order, a = rs/pq
+//      (non-positive curvature: the column errs and the solve stops),
+//      r -= a*q over its share, r.r partials per CTA
+//   4  every CTA reduces r.r, applies the stop test / budget, b = rs'/rs,
+//      then x += a*p and p = r + b*p over its share
+// Every CTA derives the same per-column scalars from the same partials in
+// the same order (no broadcast step), so results are run-to-run
+// deterministic; CTA 0 publishes the per-column state for the reports.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -25,8 +27,10 @@
 namespace kz {
 
 constexpr int kSmallCgThreads = 256;
-constexpr int kSmallCgMaxCols = 256;  // columns (bpad) the fused loop handles
-constexpr size_t kSmallCgElems = size_t(1) << 22;  // block size (doubles) up to which the loop is fused
+constexpr int kSmallCgMaxCols = 256;                   // columns (bpad) the fused loop handles
+constexpr size_t kSmallCgElems = size_t(1) << 22;      // block size (doubles) up to which it is used
+constexpr int64_t kSmallCgMaxNnz = int64_t(1) << 24;   // ... and operator entries
+constexpr int kSmallCgUnroll = 8;                      // gathers in flight per lane
 
 struct SmallCgArgs {
     int32_t rows, nchunks, b, bpad;
@@ -34,43 +38,89 @@ struct SmallCgArgs {
     const int32_t* colidx;
     double beta;
     double *x, *r, *p, *q;  // chunked blocks [nchunks][rows][C]
-    double* part;           // [2][gridDim.x][bpad] CTA partials (phase 1 / phase 2 buffers)
+    double* part;           // [2][gridDim.x][bpad] CTA partials (two phases in flight)
+    double* carry;          // [2][nwarps][bpad] split-row partials: last row / first row of a warp
     SolveState s;
 };
 
-// first row whose cost rowptr[i] + i reaches `target` (rows in [0, n])
-__device__ __forceinline__ int32_t cost_row(const int32_t* rowptr, int32_t n, int64_t target) {
+// the row holding merged position pos (row i starts at rowptr[i] + i): the
+// largest i with rowptr[i] + i <= pos
+__device__ __forceinline__ int32_t merge_row(const int32_t* rowptr, int32_t n, int64_t pos) {
     int32_t lo = 0, hi = n;
     while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        if (static_cast<int64_t>(rowptr[mid]) + mid < target) lo = mid + 1;
-        else hi = mid;
+        const int32_t mid = (lo + hi + 1) >> 1;
+        if (static_cast<int64_t>(rowptr[mid]) + mid <= pos) lo = mid;
+        else hi = mid - 1;
     }
     return lo;
+}
+
+// the warp whose merge-path share [total*w/nw, total*(w+1)/nw) holds pos
+__device__ __forceinline__ int warp_of(int64_t pos, int64_t total, int nw) {
+    int w = static_cast<int>(pos * nw / total);
+    while (w + 1 < nw && total * (w + 1) / nw <= pos) ++w;
+    while (w > 0 && total * w / nw > pos) --w;
+    return w;
+}
+
+// sum of Xc rows colidx[e] (e in [e0, e1), every NS-th from e0 + st) for
+// column col, kSmallCgUnroll gathers in flight, fixed order; the NS streams
+// are combined by a fixed butterfly
+template <int C, int NS>
+__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ colidx, int32_t e0, int32_t e1, int st,
+                                             int col, const double* __restrict__ Xc) {
+    constexpr int U = kSmallCgUnroll;
+    double acc = 0.0;
+    int32_t e = e0 + st;
+    for (; e + (U - 1) * NS < e1; e += U * NS) {
+        int32_t j[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = __ldg(colidx + e + u * NS);
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcg(Xc + static_cast<size_t>(j[u]) * C + col);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u];
+    }
+    for (; e < e1; e += NS) acc += __ldcg(Xc + static_cast<size_t>(__ldg(colidx + e)) * C + col);
+#pragma unroll
+    for (int off = C; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    return acc;
 }
 
 template <int C>
 __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a) {
     namespace cgr = cooperative_groups;
     cgr::grid_group grid = cgr::this_grid();
-    constexpr int NS = 32 / C;  // neighbour streams per warp (lanes of one stream = the C columns)
+    constexpr int NS = 32 / C;  // neighbour streams per warp; lane % C = column
     constexpr int WPC = kSmallCgThreads / 32;
     __shared__ double s_red[kSmallCgThreads];
     __shared__ double s_a[kSmallCgMaxCols], s_b[kSmallCgMaxCols], s_rs[kSmallCgMaxCols];
-    __shared__ int s_on[kSmallCgMaxCols], s_act[kSmallCgMaxCols], s_chunk[kSmallCgMaxCols / 1];
+    __shared__ int s_on[kSmallCgMaxCols], s_act[kSmallCgMaxCols], s_chunk[kSmallCgMaxCols];
     __shared__ int s_any, s_err;
     const SolveState& s = a.s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPC + warp, nw = gridDim.x * WPC;
     const int64_t ld = static_cast<int64_t>(a.rows) * C;
     const int nch = a.nchunks, bpad = a.bpad;
-    // cost-balanced row segment of this warp
+    const int col = lane % C, st = lane / C;
+    // merge-path share [S, E) of this warp; rows rs0 .. rs1 intersect it
     const int64_t total = static_cast<int64_t>(a.rowptr[a.rows]) + a.rows;
-    const int32_t r0 = cost_row(a.rowptr, a.rows, total * gw / nw);
-    const int32_t r1 = cost_row(a.rowptr, a.rows, total * (gw + 1) / nw);
+    const int64_t S = total * gw / nw, E = total * (gw + 1) / nw;
+    const bool has = S < E;
+    const int32_t rs0 = has ? merge_row(a.rowptr, a.rows, S) : 0;
+    const int32_t rs1 = has ? merge_row(a.rowptr, a.rows, E - 1) : -1;
+    auto row_start = [&](int32_t i) { return static_cast<int64_t>(a.rowptr[i]) + i; };
+    auto row_endpos = [&](int32_t i) { return static_cast<int64_t>(a.rowptr[i + 1]) + i; };  // the row-end item
+    const bool first_split = has && row_start(rs0) < S && row_endpos(rs0) < E;  // finish rs0 after the barrier
+    double* carry_last = a.carry;
+    double* carry_first = a.carry + static_cast<size_t>(nw) * bpad;
     // element share of this CTA inside each chunk: rows [e0, e1)
     const int32_t e0 = static_cast<int32_t>(static_cast<int64_t>(a.rows) * blockIdx.x / gridDim.x);
     const int32_t e1 = static_cast<int32_t>(static_cast<int64_t>(a.rows) * (blockIdx.x + 1) / gridDim.x);
+    double* partA = a.part;
+    double* partB = a.part + static_cast<size_t>(gridDim.x) * bpad;
+
     for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
         s_act[c] = c < a.b ? s.active[c] : 0;
         s_rs[c] = s.rs[c];
@@ -89,66 +139,97 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         }
         __syncthreads();
     };
-    // CTA partial (threads sharing a column add in fixed order) -> part[cta][col]
-    // two partial buffers: a CTA that has finished reducing buffer A may
-    // write buffer B while slower CTAs still read A (and vice versa a phase
-    // later); a grid barrier separates every reuse of one buffer
-    double* partA = a.part;
-    double* partB = a.part + static_cast<size_t>(gridDim.x) * bpad;
-    auto cta_partial = [&](double v, int chunk) {
+    // per-thread values of one chunk (thread t holds column t % C) -> CTA partial
+    auto cta_partial = [&](double v, int chunk, double* part) {
         s_red[threadIdx.x] = v;
         __syncthreads();
         if (threadIdx.x < C) {
             double t = 0.0;
             for (int k = threadIdx.x; k < kSmallCgThreads; k += C) t += s_red[k];
-            partB[static_cast<size_t>(blockIdx.x) * bpad + chunk * C + threadIdx.x] = t;
+            part[static_cast<size_t>(blockIdx.x) * bpad + chunk * C + threadIdx.x] = t;
         }
         __syncthreads();
     };
-    // every CTA: column totals of the CTA partials, fixed order
+    // every CTA: the column totals of the CTA partials, in a fixed order
+    // (TPC threads per column sum strided subsets, then a fixed tree)
     auto reduce_cols = [&](const double* part, double* out) {
-        for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
-            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-            int k = 0;
-            for (; k + 3 < static_cast<int>(gridDim.x); k += 4) {
-                t0 += __ldcg(part + static_cast<size_t>(k) * bpad + c);
-                t1 += __ldcg(part + static_cast<size_t>(k + 1) * bpad + c);
-                t2 += __ldcg(part + static_cast<size_t>(k + 2) * bpad + c);
-                t3 += __ldcg(part + static_cast<size_t>(k + 3) * bpad + c);
+        int TPC = 1;
+        while (TPC * 2 * bpad <= kSmallCgThreads) TPC *= 2;
+        const int G = static_cast<int>(gridDim.x);
+        for (int base = 0; base < bpad; base += kSmallCgThreads / TPC) {
+            const int c = base + static_cast<int>(threadIdx.x) / TPC, sub = threadIdx.x % TPC;
+            double t0 = 0.0, t1 = 0.0;
+            if (c < bpad) {
+                int k = sub;
+                for (; k + TPC < G; k += 2 * TPC) {
+                    t0 += __ldcg(part + static_cast<size_t>(k) * bpad + c);
+                    t1 += __ldcg(part + static_cast<size_t>(k + TPC) * bpad + c);
+                }
+                if (k < G) t0 += __ldcg(part + static_cast<size_t>(k) * bpad + c);
             }
-            for (; k < static_cast<int>(gridDim.x); ++k) t0 += __ldcg(part + static_cast<size_t>(k) * bpad + c);
-            out[c] = (t0 + t1) + (t2 + t3);
+            s_red[threadIdx.x] = t0 + t1;
+            __syncthreads();
+            for (int w = TPC / 2; w > 0; w >>= 1) {
+                if (sub < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
+                __syncthreads();
+            }
+            if (sub == 0 && c < bpad) out[c] = s_red[threadIdx.x];
+            __syncthreads();
         }
-        __syncthreads();
     };
     chunk_flags();
     int64_t it = 0;
     for (;;) {
         if (!s_any || it >= s.max_iter) break;
         ++it;
-        // ---- phase 1: q = p - beta*A p, warp partials of p.q -> CTA partials
+        // ---- phase 1: gathers over the merge-path share; split-row partials
         for (int ch = 0; ch < nch; ++ch) {
-            double dot = 0.0;
-            if (s_chunk[ch]) {
-                const double* pc = a.p + static_cast<size_t>(ch) * ld;
-                double* qc = a.q + static_cast<size_t>(ch) * ld;
-                const int col = lane % C, st = lane / C;
-                for (int32_t i = r0; i < r1; ++i) {
-                    const int32_t beg = a.rowptr[i], end = a.rowptr[i + 1];
-                    double acc = 0.0;
-                    for (int32_t e = beg + st; e < end; e += NS)
-                        acc += pc[static_cast<size_t>(a.colidx[e]) * C + col];
-#pragma unroll
-                    for (int off = C; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                    if (st == 0) {
-                        const double pv = pc[static_cast<size_t>(i) * C + col];
-                        const double qv = __dadd_rn(pv, __dmul_rn(-a.beta, acc));
-                        qc[static_cast<size_t>(i) * C + col] = qv;
-                        dot = fma(pv, qv, dot);
-                    }
+            if (!s_chunk[ch] || !has) continue;
+            const double* pc = a.p + static_cast<size_t>(ch) * ld;
+            double* qc = a.q + static_cast<size_t>(ch) * ld;
+            for (int32_t i = rs0; i <= rs1; ++i) {
+                const int32_t beg = static_cast<int32_t>(max(static_cast<int64_t>(a.rowptr[i]), S - i));
+                const int32_t end = static_cast<int32_t>(min(static_cast<int64_t>(a.rowptr[i + 1]), E - i));
+                const double acc = gather_sum<C, NS>(a.colidx, beg, end, st, col, pc);
+                if (st != 0) continue;
+                const bool own = row_endpos(i) < E, start = row_start(i) >= S;
+                const size_t slot = static_cast<size_t>(gw) * bpad + ch * C + col;
+                if (own && start) {  // the whole row is here: finish it now
+                    const double pv = __ldcg(pc + static_cast<size_t>(i) * C + col);
+                    qc[static_cast<size_t>(i) * C + col] = __dadd_rn(pv, __dmul_rn(-a.beta, acc));
+                } else if (!own) {  // continues in the next warp(s): its part of the sum
+                    carry_last[slot] = acc;
+                } else {  // ends here, started earlier: finished after the barrier
+                    carry_first[slot] = acc;
                 }
             }
-            // warp partial (lanes < C) -> CTA partial, warps in fixed order
+        }
+        __threadfence();
+        grid.sync();
+        // ---- phase 2: finish split rows (partials in warp order), p.q partials
+        for (int ch = 0; ch < nch; ++ch) {
+            double dot = 0.0;
+            if (s_chunk[ch] && has && st == 0) {
+                const double* pc = a.p + static_cast<size_t>(ch) * ld;
+                double* qc = a.q + static_cast<size_t>(ch) * ld;
+                if (first_split) {
+                    // warps w0 .. gw-1 hold the earlier parts of row rs0
+                    const int w0 = warp_of(row_start(rs0), total, nw);
+                    double acc = 0.0;
+                    for (int w = w0; w < gw; ++w)  // (warps with an empty share hold no part)
+                        if (total * (w + 1) / nw > total * w / nw)
+                            acc += __ldcg(carry_last + static_cast<size_t>(w) * bpad + ch * C + col);
+                    acc += __ldcg(carry_first + static_cast<size_t>(gw) * bpad + ch * C + col);
+                    const double pv = __ldcg(pc + static_cast<size_t>(rs0) * C + col);
+                    qc[static_cast<size_t>(rs0) * C + col] = __dadd_rn(pv, __dmul_rn(-a.beta, acc));
+                }
+                // p.q over the rows whose end this warp owns
+                for (int32_t i = rs0; i <= rs1; ++i) {
+                    if (row_endpos(i) >= E) continue;
+                    const double pv = __ldcg(pc + static_cast<size_t>(i) * C + col);
+                    dot = fma(pv, __ldcg(qc + static_cast<size_t>(i) * C + col), dot);
+                }
+            }
             if (lane >= C) dot = 0.0;
             s_red[threadIdx.x] = dot;
             __syncthreads();
@@ -161,14 +242,14 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         }
         __threadfence();
         grid.sync();
-        // ---- phase 2: a = rs / pq, r -= a*q, CTA partials of r.r
+        // ---- phase 3: a = rs / pq, r -= a*q, r.r partials
         reduce_cols(partA, s_a);  // s_a := pq
         if (threadIdx.x == 0) s_err = 0;
         __syncthreads();
         for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
             const double pq = s_a[c];
             int on = s_act[c];
-            if (on && pq <= 0.0) {
+            if (on && pq <= 0.0) {  // solver.py:84-85
                 on = 0;
                 s_act[c] = 0;
                 atomicExch(&s_err, 1);
@@ -186,32 +267,32 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
             break;
         }
         for (int ch = 0; ch < nch; ++ch) {
-            const int col = ch * C + threadIdx.x % C;
+            const int cc = ch * C + threadIdx.x % C;
             double rr = 0.0;
             if (s_chunk[ch]) {
                 double* rc = a.r + static_cast<size_t>(ch) * ld;
                 const double* qc = a.q + static_cast<size_t>(ch) * ld;
-                const double av = s_a[col];
-                const bool on = s_on[col] != 0;
+                const double av = s_a[cc];
+                const bool on = s_on[cc] != 0;
                 for (int64_t e = static_cast<int64_t>(e0) * C + threadIdx.x; e < static_cast<int64_t>(e1) * C;
                      e += kSmallCgThreads) {
-                    double rv = rc[e];
+                    double rv = __ldcg(rc + e);
                     if (on) {
-                        rv = __dsub_rn(rv, __dmul_rn(av, qc[e]));
+                        rv = __dsub_rn(rv, __dmul_rn(av, __ldcg(qc + e)));
                         rc[e] = rv;
                     }
                     rr = fma(rv, rv, rr);
                 }
             }
-            cta_partial(rr, ch);
+            cta_partial(rr, ch, partB);
         }
         __threadfence();
         grid.sync();
-        // ---- phase 3: stop test, b = rs'/rs, x += a*p, p = r + b*p
+        // ---- phase 4: stop test, b = rs'/rs, x += a*p, p = r + b*p
         reduce_cols(partB, s_b);  // s_b := r.r
         for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
             double bc = 0.0;
-            if (s_on[c]) {
+            if (s_on[c]) {  // solver.py:89-95
                 const double v = s_b[c];
                 const double rn = sqrt(v);
                 if (blockIdx.x == 0) {
@@ -237,18 +318,18 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         __syncthreads();
         for (int ch = 0; ch < nch; ++ch) {
             if (!s_chunk[ch]) continue;
-            const int col = ch * C + threadIdx.x % C;
-            const bool ox = s_on[col] != 0, op = ox && s_act[col];
+            const int cc = ch * C + threadIdx.x % C;
+            const bool ox = s_on[cc] != 0, op = ox && s_act[cc];
             if (!ox) continue;
             double* xc = a.x + static_cast<size_t>(ch) * ld;
             double* pc = a.p + static_cast<size_t>(ch) * ld;
             const double* rc = a.r + static_cast<size_t>(ch) * ld;
-            const double av = s_a[col], bv = s_b[col];
+            const double av = s_a[cc], bv = s_b[cc];
             for (int64_t e = static_cast<int64_t>(e0) * C + threadIdx.x; e < static_cast<int64_t>(e1) * C;
                  e += kSmallCgThreads) {
-                const double pv = pc[e];
-                xc[e] = __dadd_rn(xc[e], __dmul_rn(av, pv));
-                if (op) pc[e] = __dadd_rn(rc[e], __dmul_rn(bv, pv));
+                const double pv = __ldcg(pc + e);
+                xc[e] = __dadd_rn(__ldcg(xc + e), __dmul_rn(av, pv));
+                if (op) pc[e] = __dadd_rn(__ldcg(rc + e), __dmul_rn(bv, pv));
             }
         }
         chunk_flags();
@@ -258,18 +339,19 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
     if (blockIdx.x == 0 && threadIdx.x == 0) *s.n_active = 0;
 }
 
-// Grid of the fused loop: one CTA per SM at most, fewer for tiny problems;
-// 0 when the fused loop does not apply (then the caller uses the normal loop).
-inline int small_cg_grid(int64_t rows, int C, int bpad, const void* kernel) {
-    if (bpad > kSmallCgMaxCols || (kSmallCgThreads % C) != 0) return 0;
+// Grid of the fused loop (at most one CTA per SM), or 0 when it does not apply.
+inline int small_cg_grid(int64_t rows, int64_t nnz, int C, int bpad, const void* kernel) {
+    if (bpad > kSmallCgMaxCols || (kSmallCgThreads % C) != 0 || nnz > kSmallCgMaxNnz ||
+        static_cast<size_t>(rows) * bpad > kSmallCgElems)
+        return 0;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSmallCgThreads, 0) != cudaSuccess ||
         per_sm < 1) {
         cudaGetLastError();
         return 0;
     }
-    const int64_t want = std::max<int64_t>(1, (rows * bpad) / 4096);
-    return static_cast<int>(std::min<int64_t>(static_cast<int64_t>(num_sms()) * std::min(per_sm, 1), want));
+    const int64_t want = std::max<int64_t>(1, (nnz + rows) / 512);
+    return static_cast<int>(std::min<int64_t>(num_sms(), want));
 }
 
 }  // namespace kz
