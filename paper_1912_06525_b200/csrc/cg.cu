@@ -62,6 +62,7 @@ struct CgWork {
     double* y;       // eigen start: [nch][ldr][C] Galerkin coefficients
     double* small_part;   // fused small loop (cgsmall.cuh): [2][SMs][bpad] CTA partials
     double* small_carry;  // ... and [2][SMs * 8 warps][bpad] split-row partials
+    double* small_wdot;   // ... and [SMs * 8 warps][bpad] warp p.q partials
 };
 
 void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* eig = nullptr) {
@@ -119,6 +120,7 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
     w.small_part = cv.take<double>(2 * static_cast<size_t>(num_sms()) * w.bpad);
     w.small_carry = cv.take<double>(2 * static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
+    w.small_wdot = cv.take<double>(static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
 }
 
 
@@ -497,6 +499,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         sa.q = w.q;
         sa.part = w.small_part;
         sa.carry = w.small_carry;
+        sa.wdot = w.small_wdot;
         sa.s = s;
         void* kargs[] = {&sa};
         KZ_DISPATCH_C(C, KZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(cg_small_kernel<CC>),

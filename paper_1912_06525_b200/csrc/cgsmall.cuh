@@ -6,8 +6,9 @@
 //
 // Per iteration, exactly the reference recurrence of cg() (solver.py:78-95)
 // for every column:
-//   1  q = p - beta*A p over a merge-path share of (rows + entries) per warp,
-//      8 gathers in flight per lane; a row split across warps leaves carries
+//   1  q = p - beta*A p over a merge-path share of (rows + entries) per warp
+//      (K1's pipelined row gathers, coherent L2 loads); a row split across
+//      warps leaves carries
 //   2  the warp that owns a split row's end adds the carries (warp order) and
 //      finishes it; p.q partials per CTA
 //   3  every CTA reduces the CTA partials in a fixed order, a = rs/pq
@@ -30,7 +31,6 @@ constexpr int kSmallCgThreads = 256;
 constexpr int kSmallCgMaxCols = 256;                   // columns (bpad) the fused loop handles
 constexpr size_t kSmallCgElems = size_t(1) << 22;      // block size (doubles) up to which it is used
 constexpr int64_t kSmallCgMaxNnz = int64_t(1) << 24;   // ... and operator entries
-constexpr int kSmallCgUnroll = 8;                      // gathers in flight per lane
 
 struct SmallCgArgs {
     int32_t rows, nchunks, b, bpad;
@@ -40,6 +40,7 @@ struct SmallCgArgs {
     double *x, *r, *p, *q;  // chunked blocks [nchunks][rows][C]
     double* part;           // [2][gridDim.x][bpad] CTA partials (two phases in flight)
     double* carry;          // [2][nwarps][bpad] split-row partials: last row / first row of a warp
+    double* wdot;           // [nwarps][bpad] warp p.q partials (phase 1 -> phase 2)
     SolveState s;
 };
 
@@ -63,38 +64,13 @@ __device__ __forceinline__ int warp_of(int64_t pos, int64_t total, int nw) {
     return w;
 }
 
-// sum of Xc rows colidx[e] (e in [e0, e1), every NS-th from e0 + st) for
-// column col, kSmallCgUnroll gathers in flight, fixed order; the NS streams
-// are combined by a fixed butterfly
-template <int C, int NS>
-__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ colidx, int32_t e0, int32_t e1, int st,
-                                             int col, const double* __restrict__ Xc) {
-    constexpr int U = kSmallCgUnroll;
-    double acc = 0.0;
-    int32_t e = e0 + st;
-    for (; e + (U - 1) * NS < e1; e += U * NS) {
-        int32_t j[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) j[u] = __ldg(colidx + e + u * NS);
-        double v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcg(Xc + static_cast<size_t>(j[u]) * C + col);
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc += v[u];
-    }
-    for (; e < e1; e += NS) acc += __ldcg(Xc + static_cast<size_t>(__ldg(colidx + e)) * C + col);
-#pragma unroll
-    for (int off = C; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    return acc;
-}
-
 template <int C>
 __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a) {
     namespace cgr = cooperative_groups;
     cgr::grid_group grid = cgr::this_grid();
-    constexpr int NS = 32 / C;  // neighbour streams per warp; lane % C = column
     constexpr int WPC = kSmallCgThreads / 32;
     __shared__ double s_red[kSmallCgThreads];
+    __shared__ double s_red2[(kSmallCgThreads / 32) * 32];  // [warp][C] group-0 column partials
     __shared__ double s_a[kSmallCgMaxCols], s_b[kSmallCgMaxCols], s_rs[kSmallCgMaxCols];
     __shared__ int s_on[kSmallCgMaxCols], s_act[kSmallCgMaxCols], s_chunk[kSmallCgMaxCols];
     __shared__ int s_any, s_err;
@@ -103,7 +79,10 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
     const int gw = blockIdx.x * WPC + warp, nw = gridDim.x * WPC;
     const int64_t ld = static_cast<int64_t>(a.rows) * C;
     const int nch = a.nchunks, bpad = a.bpad;
-    const int col = lane % C, st = lane / C;
+    using K = Cfg<C>;
+    constexpr int VEC = K::VEC;
+    const int lg = lane % K::G, grp = lane / K::G, gbase = grp * K::G;
+    const unsigned gmask = (K::G == 32) ? 0xffffffffu : (((1u << K::G) - 1u) << gbase);
     // merge-path share [S, E) of this warp; rows rs0 .. rs1 intersect it
     const int64_t total = static_cast<int64_t>(a.rowptr[a.rows]) + a.rows;
     const int64_t S = total * gw / nw, E = total * (gw + 1) / nw;
@@ -182,60 +161,104 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
     for (;;) {
         if (!s_any || it >= s.max_iter) break;
         ++it;
-        // ---- phase 1: gathers over the merge-path share; split-row partials
+        // ---- phase 1: gathers over the merge-path share; split-row partials.
+        // Rows wholly inside the share run one per lane group (K1's short-row
+        // gather: R neighbours in flight, next indices prefetched); the split
+        // pieces at either end run across the whole warp.
         for (int ch = 0; ch < nch; ++ch) {
             if (!s_chunk[ch] || !has) continue;
             const double* pc = a.p + static_cast<size_t>(ch) * ld;
             double* qc = a.q + static_cast<size_t>(ch) * ld;
-            for (int32_t i = rs0; i <= rs1; ++i) {
-                const int32_t beg = static_cast<int32_t>(max(static_cast<int64_t>(a.rowptr[i]), S - i));
-                const int32_t end = static_cast<int32_t>(min(static_cast<int64_t>(a.rowptr[i + 1]), E - i));
-                const double acc = gather_sum<C, NS>(a.colidx, beg, end, st, col, pc);
-                if (st != 0) continue;
-                const bool own = row_endpos(i) < E, start = row_start(i) >= S;
-                const size_t slot = static_cast<size_t>(gw) * bpad + ch * C + col;
-                if (own && start) {  // the whole row is here: finish it now
-                    const double pv = __ldcg(pc + static_cast<size_t>(i) * C + col);
-                    qc[static_cast<size_t>(i) * C + col] = __dadd_rn(pv, __dmul_rn(-a.beta, acc));
-                } else if (!own) {  // continues in the next warp(s): its part of the sum
-                    carry_last[slot] = acc;
-                } else {  // ends here, started earlier: finished after the barrier
-                    carry_first[slot] = acc;
+            double dot[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) dot[v] = 0.0;
+            const bool start0 = row_start(rs0) >= S;
+            const int32_t in0 = start0 ? rs0 : rs0 + 1;
+            const int32_t in1 = row_endpos(rs1) < E ? rs1 : rs1 - 1;
+            for (int32_t i = in0 + grp; i <= in1; i += K::NGW) {
+                double acc[VEC];
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+                gather_rows<C, false, true>(a.colidx, a.rowptr[i], a.rowptr[i + 1], K::R, pc, lg, gbase, gmask, acc);
+                double pv[VEC], qv[VEC];
+                ld_cg_vec<VEC>(pc + static_cast<size_t>(i) * C + lg * VEC, pv);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    qv[v] = __dadd_rn(pv[v], __dmul_rn(-a.beta, acc[v]));
+                    dot[v] = fma(pv[v], qv[v], dot[v]);
                 }
+                st_plain<VEC>(qc + static_cast<size_t>(i) * C + lg * VEC, qv);
             }
+            // split pieces (whole warp): the tail of a row that started
+            // earlier, or the head of a row that continues
+            auto piece = [&](int32_t i, int32_t beg, int32_t end, double* dst) {
+                double acc[VEC];
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+                gather_rows<C, false, true>(a.colidx, beg + grp * K::R, end, K::NGW * K::R, pc, lg, gbase, gmask, acc);
+#pragma unroll
+                for (int off = K::G; off < 32; off <<= 1)
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+                if (grp == 0) st_plain<VEC>(dst + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, acc);
+                (void)i;
+            };
+            if (!start0)
+                piece(rs0, static_cast<int32_t>(S - rs0), static_cast<int32_t>(min(static_cast<int64_t>(a.rowptr[rs0 + 1]), E - rs0)),
+                      row_endpos(rs0) < E ? carry_first : carry_last);
+            if (row_endpos(rs1) >= E && (rs1 > rs0 || start0))
+                piece(rs1, a.rowptr[rs1], static_cast<int32_t>(E - rs1), carry_last);
+            // this warp's p.q partial of the finished rows -> wdot
+#pragma unroll
+            for (int off = K::G; off < 32; off <<= 1)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) dot[v] += __shfl_xor_sync(0xffffffffu, dot[v], off);
+            if (grp == 0) st_plain<VEC>(a.wdot + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, dot);
         }
         __threadfence();
         grid.sync();
         // ---- phase 2: finish split rows (partials in warp order), p.q partials
         for (int ch = 0; ch < nch; ++ch) {
-            double dot = 0.0;
-            if (s_chunk[ch] && has && st == 0) {
-                const double* pc = a.p + static_cast<size_t>(ch) * ld;
-                double* qc = a.q + static_cast<size_t>(ch) * ld;
+            double dot[VEC];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) dot[v] = 0.0;
+            if (s_chunk[ch] && has && grp == 0) {
+                ld_cg_vec<VEC>(a.wdot + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, dot);
                 if (first_split) {
+                    const double* pc = a.p + static_cast<size_t>(ch) * ld;
+                    double* qc = a.q + static_cast<size_t>(ch) * ld;
                     // warps w0 .. gw-1 hold the earlier parts of row rs0
                     const int w0 = warp_of(row_start(rs0), total, nw);
-                    double acc = 0.0;
+                    double acc[VEC], t[VEC];
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
                     for (int w = w0; w < gw; ++w)  // (warps with an empty share hold no part)
-                        if (total * (w + 1) / nw > total * w / nw)
-                            acc += __ldcg(carry_last + static_cast<size_t>(w) * bpad + ch * C + col);
-                    acc += __ldcg(carry_first + static_cast<size_t>(gw) * bpad + ch * C + col);
-                    const double pv = __ldcg(pc + static_cast<size_t>(rs0) * C + col);
-                    qc[static_cast<size_t>(rs0) * C + col] = __dadd_rn(pv, __dmul_rn(-a.beta, acc));
-                }
-                // p.q over the rows whose end this warp owns
-                for (int32_t i = rs0; i <= rs1; ++i) {
-                    if (row_endpos(i) >= E) continue;
-                    const double pv = __ldcg(pc + static_cast<size_t>(i) * C + col);
-                    dot = fma(pv, __ldcg(qc + static_cast<size_t>(i) * C + col), dot);
+                        if (total * (w + 1) / nw > total * w / nw) {
+                            ld_cg_vec<VEC>(carry_last + static_cast<size_t>(w) * bpad + ch * C + lg * VEC, t);
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) acc[v] += t[v];
+                        }
+                    ld_cg_vec<VEC>(carry_first + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, t);
+                    double pv[VEC], qv[VEC];
+                    ld_cg_vec<VEC>(pc + static_cast<size_t>(rs0) * C + lg * VEC, pv);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) {
+                        acc[v] += t[v];
+                        qv[v] = __dadd_rn(pv[v], __dmul_rn(-a.beta, acc[v]));
+                        dot[v] = fma(pv[v], qv[v], dot[v]);
+                    }
+                    st_plain<VEC>(qc + static_cast<size_t>(rs0) * C + lg * VEC, qv);
                 }
             }
-            if (lane >= C) dot = 0.0;
-            s_red[threadIdx.x] = dot;
+            // CTA partial over the warps in order (lanes of group 0 hold the columns)
+            if (grp == 0) {  // group 0's lanes cover the C columns
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) s_red2[warp * C + lg * VEC + v] = dot[v];
+            }
             __syncthreads();
             if (threadIdx.x < C) {
                 double t = 0.0;
-                for (int w = 0; w < WPC; ++w) t += s_red[w * 32 + threadIdx.x];
+                for (int w = 0; w < WPC; ++w) t += s_red2[w * C + threadIdx.x];
                 partA[static_cast<size_t>(blockIdx.x) * bpad + ch * C + threadIdx.x] = t;
             }
             __syncthreads();

@@ -214,7 +214,25 @@ __device__ __forceinline__ void st_stream(double* p, const double (&v)[VEC]) {
 // Sum Xg rows of neighbours col[beg..end) into acc, R neighbours per round,
 // rounds `stride` apart.  All lanes of a group share the neighbour; lane lg
 // owns columns lg*VEC .. lg*VEC+VEC-1 of the chunk.  W: weighted operator.
-template <int C, bool W = false>
+// coherent (L2) gather for kernels that also write the gathered block
+// within the same launch (the fused small CG loop): .cg loads never return a
+// stale L1 / non-coherent-cache copy across its grid barriers
+template <int VEC>
+__device__ __forceinline__ void ld_cg_vec(const double* p, double (&v)[VEC]) {
+    if constexpr (VEC == 4) {
+        asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(p));
+    } else if constexpr (VEC == 2) {
+        const double2 t = __ldcg(reinterpret_cast<const double2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+        v[0] = __ldcg(p);
+    }
+}
+
+template <int C, bool W = false, bool CO = false>
 __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int beg, int end,
                                             int stride, const double* __restrict__ Xc, int lg,
                                             int gbase, unsigned gmask,
@@ -269,7 +287,10 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
             else
                 ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #else
-            ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
+            if constexpr (CO)
+                ld_cg_vec<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
+            else
+                ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #endif
         }
         const int nvalid = end - base;  // slots t < nvalid hold real neighbours
