@@ -267,6 +267,11 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         grid.sync();
         // ---- phase 3: a = rs / pq, r -= a*q, r.r partials
         reduce_cols(partA, s_a);  // s_a := pq
+#ifdef KZ_SMALL_DEBUG
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            printf("it %lld pq0 %g rs0 %g act0 %d grid %d nw %d total %lld\n", (long long)it, s_a[0], s_rs[0], s_act[0],
+                   (int)gridDim.x, nw, (long long)total);
+#endif
         if (threadIdx.x == 0) s_err = 0;
         __syncthreads();
         for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
