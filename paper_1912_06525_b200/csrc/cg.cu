@@ -193,7 +193,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         }
     }
     const bool fused = small_grid > 0;
-    const bool use_graphs = !fused && use_graph_loop(work);
+    const bool use_graphs = !fused && use_graph_loop(work, kGraphWorkCg);
     // residual-history mode (blockops.cuh CgHistory): x is formed at the end
     // from the kept residuals instead of being updated every iteration
     const bool hist = w.H >= 3 && !use_graphs && !fused;

@@ -111,7 +111,12 @@ struct StreamScope {
 // graph launch for the whole loop: no per-iteration host work or polling.
 // Used for solves whose per-iteration work is small (launch-bound: cfg1,
 // cfg2); KZ_GRAPHS=0 turns it off, KZ_GRAPHS=1 forces it on.
-constexpr double kGraphWork = 2e9;  // (nnz + n) * columns per iteration
+// per-iteration work ((entries + rows) * columns) up to which a loop runs as
+// a graph: CG iterations above ~5e7 take >= ~100 us of device time, where the
+// host-driven residual-history loop (6 block passes, sparse first iteration)
+// wins over the graph's direction form (cfg2: 2.2 vs 3.7 ms)
+constexpr double kGraphWorkCg = 5e7;
+constexpr double kGraphWorkLrc = 2e9;
 inline int graphs_mode() {
     static const int m = [] {
         const char* e = std::getenv("KZ_GRAPHS");
@@ -119,9 +124,9 @@ inline int graphs_mode() {
     }();
     return m;
 }
-inline bool use_graph_loop(double work) {
+inline bool use_graph_loop(double work, double limit) {
     const int m = graphs_mode();
-    return m == 1 || (m == -1 && work <= kGraphWork);
+    return m == 1 || (m == -1 && work <= limit);
 }
 
 struct GraphKey {

@@ -458,7 +458,7 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
         int64_t ran = 0;
         // launch-bound small solves: the whole PCG loop is one cached graph
         // with a device-side WHILE condition (driver.cuh)
-        if (use_graph_loop(work * w.bpad)) {
+        if (use_graph_loop(work * w.bpad, kGraphWorkLrc)) {
             GraphKey key;
             key.v[0] = h->uid;
             key.v[1] = reinterpret_cast<uint64_t>(ws);

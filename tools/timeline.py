@@ -56,3 +56,6 @@ gaps.sort(reverse=True)
 print(json.dumps({"config": a.config, "solver": a.solver, "events": len(iv), "span_ms": span / 1e3,
                   "kernel_sum_ms": busy / 1e3, "idle_ms": sum(x for x, _ in gaps) / 1e3,
                   "largest_gaps_us": [(round(x, 1), n[:40]) for x, n in gaps[:12]]}))
+if os.environ.get("KZ_TIMELINE_LIST"):
+    for s, t, name in iv:
+        print(f"{(s - first):9.1f} us  +{(t - s):8.1f} us  {name[:70]}")
