@@ -61,8 +61,9 @@ struct CgWork {
     int64_t* iperm;  // inverse output permutation (gather-based store)
     double* y;       // eigen start: [nch][ldr][C] Galerkin coefficients
     double* small_part;   // fused small loop (cgsmall.cuh): [2][SMs][bpad] CTA partials
-    double* small_carry;  // ... and [2][SMs * 8 warps][bpad] split-row partials
-    double* small_wdot;   // ... and [SMs * 8 warps][bpad] warp p.q partials
+    double* small_carry;  // ... and [SMs * 8 warps][bpad] split-row partials
+    int32_t* small_stamp; // ... and [SMs * 8 warps][nchunks] carry stamps
+    kz_report* dev_reports;  // fused small solve: the packed reports
 };
 
 void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* eig = nullptr) {
@@ -119,8 +120,9 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.iperm = cv.take<int64_t>(g->rows);
     w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
     w.small_part = cv.take<double>(2 * static_cast<size_t>(num_sms()) * w.bpad);
-    w.small_carry = cv.take<double>(2 * static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
-    w.small_wdot = cv.take<double>(static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
+    w.small_carry = cv.take<double>(static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
+    w.small_stamp = cv.take<int32_t>(static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.nchunks);
+    w.dev_reports = cv.take<kz_report>(w.bpad);
 }
 
 
@@ -174,10 +176,6 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         KZ_CUDA(cudaEventCreate(&e1));
         KZ_CUDA(cudaEventRecord(e0, st));
     }
-    // zero state + counters (contiguous from s.rs to the end of qpos)
-    KZ_CUDA(zero_span(s.rs, w.qpos, st));
-    KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nchunks, st));
-    if (int rc = zero_spmm_counters(g, nchunks, w.sp, st)) return rc;
     const size_t blk_elems = static_cast<size_t>(w.bpad) * n;
     const size_t blk_bytes = sizeof(double) * blk_elems;
     const double work = static_cast<double>(g->nnz + n) * w.bpad;
@@ -192,6 +190,56 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
                                                         reinterpret_cast<const void*>(cg_small_kernel<CC>)));
         }
     }
+    if (small_grid > 0 && !eig && !a->rhs && !a->x0 && a->qpos) {
+        // the whole query solve -- rhs, start state, iterations, output,
+        // reports -- is one cooperative launch (plus the qpos upload and the
+        // report download)
+        KZ_CUDA(cudaMemcpyAsync(w.qpos, a->qpos, sizeof(int64_t) * b, cudaMemcpyHostToDevice, st));
+        KZ_CUDA(cudaMemsetAsync(s.err, 0, sizeof(int32_t), st));
+        SmallCgArgs sa{};
+        sa.rows = static_cast<int32_t>(n);
+        sa.nchunks = nchunks;
+        sa.b = b;
+        sa.bpad = w.bpad;
+        sa.rowptr = g->rowptr;
+        sa.colidx = g->colidx;
+        sa.beta = a->beta;
+        sa.x = w.x;
+        sa.r = w.r;
+        sa.p = w.p;
+        sa.q = w.q;
+        sa.part = w.small_part;
+        sa.carry = w.small_carry;
+        sa.stamp = w.small_stamp;
+        sa.s = s;
+        sa.init = 1;
+        sa.qpos = w.qpos;
+        sa.scores = a->scores;
+        sa.perm = a->perm;
+        sa.clamp = a->clamp;
+        sa.reports = w.dev_reports;
+        void* kargs[] = {&sa};
+        KZ_DISPATCH_C(C, KZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(cg_small_kernel<CC>),
+                                                            dim3(small_grid), dim3(kSmallCgThreads), kargs, 0, st)));
+        note_launch();
+        if (a->device_ms) KZ_CUDA(cudaEventRecord(e1, st));
+        int32_t err = 0;
+        KZ_CUDA(cudaMemcpyAsync(a->reports, w.dev_reports, sizeof(kz_report) * b, cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaMemcpyAsync(&err, s.err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        KZ_CUDA(cudaStreamSynchronize(st));
+        if (a->device_ms) {
+            KZ_CUDA(cudaEventElapsedTime(a->device_ms, e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        for (int j = 0; j < b; ++j)
+            if (a->reports[j].status == KZ_ENOTSPD) return fail(KZ_ENOTSPD, "operator is not positive definite");
+        return KZ_OK;
+    }
+    // zero state + counters (contiguous from s.rs to the end of qpos)
+    KZ_CUDA(zero_span(s.rs, w.qpos, st));
+    KZ_CUDA(cudaMemsetAsync(w.red.cnt, 0, sizeof(int32_t) * nchunks, st));
+    if (int rc = zero_spmm_counters(g, nchunks, w.sp, st)) return rc;
     const bool fused = small_grid > 0;
     const bool use_graphs = !fused && use_graph_loop(work, kGraphWorkCg);
     // residual-history mode (blockops.cuh CgHistory): x is formed at the end
@@ -485,7 +533,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     long long per_iter = 0;
     int rc;
     if (fused) {
-        SmallCgArgs sa;
+        SmallCgArgs sa{};
         sa.rows = static_cast<int32_t>(n);
         sa.nchunks = nchunks;
         sa.b = b;
@@ -499,7 +547,7 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
         sa.q = w.q;
         sa.part = w.small_part;
         sa.carry = w.small_carry;
-        sa.wdot = w.small_wdot;
+        sa.stamp = w.small_stamp;
         sa.s = s;
         void* kargs[] = {&sa};
         KZ_DISPATCH_C(C, KZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(cg_small_kernel<CC>),

@@ -1,24 +1,28 @@
-// cgsmall.cuh -- the whole CG loop of a small batched solve in ONE
-// cooperative kernel.  At cfg1 sizes (n ~ 10^4, 16 columns) the vector blocks
-// sit in L2 and every kernel of the host- or graph-driven loop costs more in
-// launch, tail and cross-CTA-reduction latency than in work; here an
-// iteration is four short phases separated by grid barriers.
+// cgsmall.cuh -- a whole small batched CG solve in ONE cooperative kernel.
+// At cfg1 sizes (n ~ 10^4, 16 columns) the vector blocks sit in L2 and every
+// separate kernel, memset and copy of the host- or graph-driven loop costs
+// more in launch, tail and cross-CTA-reduction latency than in work; here the
+// right-hand side, the CG iterations, the output store and the reports are
+// one launch with three grid barriers per iteration.
 //
 // Per iteration, exactly the reference recurrence of cg() (solver.py:78-95)
 // for every column:
 //   1  q = p - beta*A p over a merge-path share of (rows + entries) per warp
-//      (K1's pipelined row gathers, coherent L2 loads); a row split across
-//      warps leaves carries
-//   2  the warp that owns a split row's end adds the carries (warp order) and
-//      finishes it; p.q partials per CTA
-//   3  every CTA reduces the CTA partials in a fixed order, a = rs/pq
+//      (K1's pipelined row gathers with coherent L2 loads); a row split
+//      across warps leaves its earlier parts as carries, published with a
+//      per-(warp, chunk) iteration stamp, and the warp owning the row's end
+//      adds them in warp order; p.q partials per CTA
+//   2  every CTA reduces the CTA partials in a fixed order, a = rs/pq
 //      (non-positive curvature: the column errs and the solve stops),
 //      r -= a*q over its share, r.r partials per CTA
-//   4  every CTA reduces r.r, applies the stop test / budget, b = rs'/rs,
+//   3  every CTA reduces r.r, applies the stop test / budget, b = rs'/rs,
 //      then x += a*p and p = r + b*p over its share
 // Every CTA derives the same per-column scalars from the same partials in
 // the same order (no broadcast step), so results are run-to-run
-// deterministic; CTA 0 publishes the per-column state for the reports.
+// deterministic; CTA 0 publishes the per-column state and the reports.
+// With `init` the kernel also forms r0 = p0 = beta*A e_q (index.py:93-101),
+// ||b|| and the start state (solver.py:71-77) itself, and with `scores` it
+// stores clamp(x) through perm (solver.py:223-225).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -31,6 +35,7 @@ constexpr int kSmallCgThreads = 256;
 constexpr int kSmallCgMaxCols = 256;                   // columns (bpad) the fused loop handles
 constexpr size_t kSmallCgElems = size_t(1) << 22;      // block size (doubles) up to which it is used
 constexpr int64_t kSmallCgMaxNnz = int64_t(1) << 24;   // ... and operator entries
+constexpr int kSmallCgWarps = kSmallCgThreads / 32;
 
 struct SmallCgArgs {
     int32_t rows, nchunks, b, bpad;
@@ -39,9 +44,17 @@ struct SmallCgArgs {
     double beta;
     double *x, *r, *p, *q;  // chunked blocks [nchunks][rows][C]
     double* part;           // [2][gridDim.x][bpad] CTA partials (two phases in flight)
-    double* carry;          // [2][nwarps][bpad] split-row partials: last row / first row of a warp
-    double* wdot;           // [nwarps][bpad] warp p.q partials (phase 1 -> phase 2)
+    double* carry;          // [nwarps][bpad] split-row partials published by each warp
+    int32_t* stamp;         // [nwarps][nchunks] iteration whose carry is published
     SolveState s;
+    // init: r0 = p0 = beta*A e_q from qpos, x0 = 0, the start state
+    int init;
+    const int64_t* qpos;    // device [b]
+    // output (scores != NULL): scores[j][perm ? perm[i] : i] = clamp(x_j[i]); reports[j]
+    double* scores;
+    const int64_t* perm;
+    int clamp;
+    kz_report* reports;     // device [b]
 };
 
 // the row holding merged position pos (row i starts at rowptr[i] + i): the
@@ -68,19 +81,18 @@ template <int C>
 __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a) {
     namespace cgr = cooperative_groups;
     cgr::grid_group grid = cgr::this_grid();
-    constexpr int WPC = kSmallCgThreads / 32;
+    using K = Cfg<C>;
+    constexpr int VEC = K::VEC;
     __shared__ double s_red[kSmallCgThreads];
-    __shared__ double s_red2[(kSmallCgThreads / 32) * 32];  // [warp][C] group-0 column partials
+    __shared__ double s_red2[kSmallCgWarps * 32];  // [warp][C] group-0 column partials
     __shared__ double s_a[kSmallCgMaxCols], s_b[kSmallCgMaxCols], s_rs[kSmallCgMaxCols];
     __shared__ int s_on[kSmallCgMaxCols], s_act[kSmallCgMaxCols], s_chunk[kSmallCgMaxCols];
     __shared__ int s_any, s_err;
     const SolveState& s = a.s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * WPC + warp, nw = gridDim.x * WPC;
+    const int gw = blockIdx.x * kSmallCgWarps + warp, nw = gridDim.x * kSmallCgWarps;
     const int64_t ld = static_cast<int64_t>(a.rows) * C;
     const int nch = a.nchunks, bpad = a.bpad;
-    using K = Cfg<C>;
-    constexpr int VEC = K::VEC;
     const int lg = lane % K::G, grp = lane / K::G, gbase = grp * K::G;
     const unsigned gmask = (K::G == 32) ? 0xffffffffu : (((1u << K::G) - 1u) << gbase);
     // merge-path share [S, E) of this warp; rows rs0 .. rs1 intersect it
@@ -91,18 +103,68 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
     const int32_t rs1 = has ? merge_row(a.rowptr, a.rows, E - 1) : -1;
     auto row_start = [&](int32_t i) { return static_cast<int64_t>(a.rowptr[i]) + i; };
     auto row_endpos = [&](int32_t i) { return static_cast<int64_t>(a.rowptr[i + 1]) + i; };  // the row-end item
-    const bool first_split = has && row_start(rs0) < S && row_endpos(rs0) < E;  // finish rs0 after the barrier
+    const bool first_split = has && row_start(rs0) < S && row_endpos(rs0) < E;  // owns the end of a split row
+    const int w0 = first_split ? warp_of(row_start(rs0), total, nw) : gw;    // ... whose start is in warp w0
     double* carry_last = a.carry;
-    double* carry_first = a.carry + static_cast<size_t>(nw) * bpad;
     // element share of this CTA inside each chunk: rows [e0, e1)
     const int32_t e0 = static_cast<int32_t>(static_cast<int64_t>(a.rows) * blockIdx.x / gridDim.x);
     const int32_t e1 = static_cast<int32_t>(static_cast<int64_t>(a.rows) * (blockIdx.x + 1) / gridDim.x);
     double* partA = a.part;
     double* partB = a.part + static_cast<size_t>(gridDim.x) * bpad;
 
+    if (a.init) {
+        // ---- r0 = p0 = beta*A e_q, x0 = 0; ||b||; the start state ----
+        for (int ch = 0; ch < nch; ++ch)
+            for (int64_t e = static_cast<int64_t>(e0) * C + threadIdx.x; e < static_cast<int64_t>(e1) * C;
+                 e += kSmallCgThreads) {
+                const size_t o = static_cast<size_t>(ch) * ld + e;
+                a.x[o] = 0.0;
+                a.r[o] = 0.0;
+                a.p[o] = 0.0;
+            }
+    }
+    // carry stamps of an earlier solve on this workspace must not match
+    for (int i = blockIdx.x * kSmallCgThreads + threadIdx.x; i < nw * nch; i += gridDim.x * kSmallCgThreads)
+        a.stamp[i] = 0;
+    __threadfence();
+    grid.sync();
+    if (a.init) {
+        for (int j = blockIdx.x; j < bpad; j += gridDim.x) {
+            const int ch = j / C, c = j % C;
+            if (j < a.b) {
+                const int64_t q = a.qpos[j];
+                const int32_t beg = a.rowptr[q], end = a.rowptr[q + 1];
+                for (int32_t e = beg + threadIdx.x; e < end; e += kSmallCgThreads) {
+                    const size_t o = static_cast<size_t>(ch) * ld + static_cast<size_t>(a.colidx[e]) * C + c;
+                    a.r[o] = a.beta;
+                    a.p[o] = a.beta;
+                }
+            }
+            if (threadIdx.x == 0) {
+                // ||b||^2 = sum over N(q) of beta^2, in CSR order (solver.py:71)
+                double bn2 = 0.0;
+                if (j < a.b) {
+                    const int32_t deg = a.rowptr[a.qpos[j] + 1] - a.rowptr[a.qpos[j]];
+                    for (int32_t k = 0; k < deg; ++k) bn2 = fma(a.beta, a.beta, bn2);
+                }
+                s.bnorm2[j] = bn2;
+                const double bn = sqrt(bn2);
+                s.thresh[j] = s.tol * bn;
+                s.rnorm[j] = bn;
+                s.rs[j] = bn2;
+                s.iters[j] = 0;
+                s.status[j] = 0;
+                const bool act = j < a.b && bn > s.thresh[j];
+                s.active[j] = act ? 1 : 0;
+                s.converged[j] = act ? 0 : 1;
+            }
+        }
+        __threadfence();
+        grid.sync();
+    }
     for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
-        s_act[c] = c < a.b ? s.active[c] : 0;
-        s_rs[c] = s.rs[c];
+        s_act[c] = c < a.b ? __ldcg(s.active + c) : 0;
+        s_rs[c] = __ldcg(s.rs + c);
     }
     __syncthreads();
     auto chunk_flags = [&]() {
@@ -130,23 +192,28 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         __syncthreads();
     };
     // every CTA: the column totals of the CTA partials, in a fixed order
-    // (TPC threads per column sum strided subsets, then a fixed tree)
+    // (TPC threads per column sum strided subsets -- all loads issued
+    // before the adds -- then a fixed tree)
     auto reduce_cols = [&](const double* part, double* out) {
         int TPC = 1;
         while (TPC * 2 * bpad <= kSmallCgThreads) TPC *= 2;
         const int G = static_cast<int>(gridDim.x);
         for (int base = 0; base < bpad; base += kSmallCgThreads / TPC) {
             const int c = base + static_cast<int>(threadIdx.x) / TPC, sub = threadIdx.x % TPC;
-            double t0 = 0.0, t1 = 0.0;
+            double t = 0.0;
             if (c < bpad) {
-                int k = sub;
-                for (; k + TPC < G; k += 2 * TPC) {
-                    t0 += __ldcg(part + static_cast<size_t>(k) * bpad + c);
-                    t1 += __ldcg(part + static_cast<size_t>(k + TPC) * bpad + c);
+                for (int k0 = sub; k0 < G; k0 += 8 * TPC) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = k0 + u * TPC;
+                        v[u] = k < G ? __ldcg(part + static_cast<size_t>(k) * bpad + c) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t += v[u];
                 }
-                if (k < G) t0 += __ldcg(part + static_cast<size_t>(k) * bpad + c);
             }
-            s_red[threadIdx.x] = t0 + t1;
+            s_red[threadIdx.x] = t;
             __syncthreads();
             for (int w = TPC / 2; w > 0; w >>= 1) {
                 if (sub < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
@@ -161,117 +228,125 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
     for (;;) {
         if (!s_any || it >= s.max_iter) break;
         ++it;
-        // ---- phase 1: gathers over the merge-path share; split-row partials.
+        // ---- phase 1: q = p - beta*A p over the merge-path share, p.q partials.
         // Rows wholly inside the share run one per lane group (K1's short-row
         // gather: R neighbours in flight, next indices prefetched); the split
         // pieces at either end run across the whole warp.
         for (int ch = 0; ch < nch; ++ch) {
-            if (!s_chunk[ch] || !has) continue;
-            const double* pc = a.p + static_cast<size_t>(ch) * ld;
-            double* qc = a.q + static_cast<size_t>(ch) * ld;
             double dot[VEC];
 #pragma unroll
             for (int v = 0; v < VEC; ++v) dot[v] = 0.0;
-            const bool start0 = row_start(rs0) >= S;
-            const int32_t in0 = start0 ? rs0 : rs0 + 1;
-            const int32_t in1 = row_endpos(rs1) < E ? rs1 : rs1 - 1;
-            for (int32_t i = in0 + grp; i <= in1; i += K::NGW) {
-                double acc[VEC];
+            if (s_chunk[ch] && has) {
+                const double* pc = a.p + static_cast<size_t>(ch) * ld;
+                double* qc = a.q + static_cast<size_t>(ch) * ld;
+                const bool start0 = row_start(rs0) >= S;
+                const int32_t in0 = start0 ? rs0 : rs0 + 1;
+                const int32_t in1 = row_endpos(rs1) < E ? rs1 : rs1 - 1;
+                auto finish = [&](int32_t i, const double (&acc)[VEC]) {  // q_i and its p.q term
+                    double pv[VEC], qv[VEC];
+                    ld_cg_vec<VEC>(pc + static_cast<size_t>(i) * C + lg * VEC, pv);
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-                gather_rows<C, false, true>(a.colidx, a.rowptr[i], a.rowptr[i + 1], K::R, pc, lg, gbase, gmask, acc);
-                double pv[VEC], qv[VEC];
-                ld_cg_vec<VEC>(pc + static_cast<size_t>(i) * C + lg * VEC, pv);
+                    for (int v = 0; v < VEC; ++v) {
+                        qv[v] = __dadd_rn(pv[v], __dmul_rn(-a.beta, acc[v]));
+                        dot[v] = fma(pv[v], qv[v], dot[v]);
+                    }
+                    st_plain<VEC>(qc + static_cast<size_t>(i) * C + lg * VEC, qv);
+                };
+                for (int32_t i = in0 + grp; i <= in1; i += K::NGW) {
+                    double acc[VEC];
 #pragma unroll
-                for (int v = 0; v < VEC; ++v) {
-                    qv[v] = __dadd_rn(pv[v], __dmul_rn(-a.beta, acc[v]));
-                    dot[v] = fma(pv[v], qv[v], dot[v]);
+                    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+                    gather_rows<C, false, true>(a.colidx, a.rowptr[i], a.rowptr[i + 1], K::R, pc, lg, gbase, gmask,
+                                                acc);
+                    finish(i, acc);
                 }
-                st_plain<VEC>(qc + static_cast<size_t>(i) * C + lg * VEC, qv);
+                // whole-warp piece of a split row, summed over the lane groups
+                auto piece = [&](int32_t beg, int32_t end, double (&acc)[VEC]) {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+                    gather_rows<C, false, true>(a.colidx, beg + grp * K::R, end, K::NGW * K::R, pc, lg, gbase, gmask,
+                                                acc);
+#pragma unroll
+                    for (int off = K::G; off < 32; off <<= 1)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+                };
+                auto publish = [&](const double (&acc)[VEC]) {  // carry_last + stamp
+                    if (grp == 0) st_plain<VEC>(carry_last + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, acc);
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) atomicExch(a.stamp + static_cast<size_t>(gw) * nch + ch, static_cast<int32_t>(it));
+                };
+                double tail[VEC];  // this warp's part of a split row it owns the end of
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) tail[v] = 0.0;
+                if (!start0) {
+                    double acc[VEC];
+                    piece(static_cast<int32_t>(S - rs0),
+                          static_cast<int32_t>(min(static_cast<int64_t>(a.rowptr[rs0 + 1]), E - rs0)), acc);
+                    if (first_split) {
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) tail[v] = acc[v];
+                    } else {
+                        publish(acc);  // a middle piece: the row continues
+                    }
+                }
+                if (row_endpos(rs1) >= E && (rs1 > rs0 || start0)) {
+                    double acc[VEC];
+                    piece(a.rowptr[rs1], static_cast<int32_t>(E - rs1), acc);  // the head of a row that continues
+                    publish(acc);
+                }
+                if (first_split) {
+                    // the earlier parts of row rs0 (warps w0 .. gw-1), in warp order;
+                    // every warp publishes before it waits, so this cannot deadlock
+                    double acc[VEC];
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+                    for (int w = w0; w < gw; ++w) {
+                        if (total * (w + 1) / nw <= total * w / nw) continue;  // an empty share holds no part
+                        if (lane == 0) {
+                            volatile int32_t* f = a.stamp + static_cast<size_t>(w) * nch + ch;
+#if KZ_CHECKED
+                            long long spins = 0;
+                            while (*f != static_cast<int32_t>(it)) KZ_DCHECK(++spins < (1ll << 28));
+#else
+                            while (*f != static_cast<int32_t>(it)) {
+                            }
+#endif
+                        }
+                        __syncwarp();
+                        __threadfence();
+                        double t[VEC];
+                        ld_cg_vec<VEC>(carry_last + static_cast<size_t>(w) * bpad + ch * C + lg * VEC, t);
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] += t[v];
+                    }
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) acc[v] += tail[v];
+                    if (grp == 0) finish(rs0, acc);
+                }
             }
-            // split pieces (whole warp): the tail of a row that started
-            // earlier, or the head of a row that continues
-            auto piece = [&](int32_t i, int32_t beg, int32_t end, double* dst) {
-                double acc[VEC];
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-                gather_rows<C, false, true>(a.colidx, beg + grp * K::R, end, K::NGW * K::R, pc, lg, gbase, gmask, acc);
-#pragma unroll
-                for (int off = K::G; off < 32; off <<= 1)
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
-                if (grp == 0) st_plain<VEC>(dst + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, acc);
-                (void)i;
-            };
-            if (!start0)
-                piece(rs0, static_cast<int32_t>(S - rs0), static_cast<int32_t>(min(static_cast<int64_t>(a.rowptr[rs0 + 1]), E - rs0)),
-                      row_endpos(rs0) < E ? carry_first : carry_last);
-            if (row_endpos(rs1) >= E && (rs1 > rs0 || start0))
-                piece(rs1, a.rowptr[rs1], static_cast<int32_t>(E - rs1), carry_last);
-            // this warp's p.q partial of the finished rows -> wdot
+            // warp p.q partial (butterfly over the lane groups) -> CTA partial, warps in order
 #pragma unroll
             for (int off = K::G; off < 32; off <<= 1)
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) dot[v] += __shfl_xor_sync(0xffffffffu, dot[v], off);
-            if (grp == 0) st_plain<VEC>(a.wdot + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, dot);
-        }
-        __threadfence();
-        grid.sync();
-        // ---- phase 2: finish split rows (partials in warp order), p.q partials
-        for (int ch = 0; ch < nch; ++ch) {
-            double dot[VEC];
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) dot[v] = 0.0;
-            if (s_chunk[ch] && has && grp == 0) {
-                ld_cg_vec<VEC>(a.wdot + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, dot);
-                if (first_split) {
-                    const double* pc = a.p + static_cast<size_t>(ch) * ld;
-                    double* qc = a.q + static_cast<size_t>(ch) * ld;
-                    // warps w0 .. gw-1 hold the earlier parts of row rs0
-                    const int w0 = warp_of(row_start(rs0), total, nw);
-                    double acc[VEC], t[VEC];
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-                    for (int w = w0; w < gw; ++w)  // (warps with an empty share hold no part)
-                        if (total * (w + 1) / nw > total * w / nw) {
-                            ld_cg_vec<VEC>(carry_last + static_cast<size_t>(w) * bpad + ch * C + lg * VEC, t);
-#pragma unroll
-                            for (int v = 0; v < VEC; ++v) acc[v] += t[v];
-                        }
-                    ld_cg_vec<VEC>(carry_first + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, t);
-                    double pv[VEC], qv[VEC];
-                    ld_cg_vec<VEC>(pc + static_cast<size_t>(rs0) * C + lg * VEC, pv);
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) {
-                        acc[v] += t[v];
-                        qv[v] = __dadd_rn(pv[v], __dmul_rn(-a.beta, acc[v]));
-                        dot[v] = fma(pv[v], qv[v], dot[v]);
-                    }
-                    st_plain<VEC>(qc + static_cast<size_t>(rs0) * C + lg * VEC, qv);
-                }
-            }
-            // CTA partial over the warps in order (lanes of group 0 hold the columns)
-            if (grp == 0) {  // group 0's lanes cover the C columns
+            if (grp == 0) {
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) s_red2[warp * C + lg * VEC + v] = dot[v];
             }
             __syncthreads();
             if (threadIdx.x < C) {
                 double t = 0.0;
-                for (int w = 0; w < WPC; ++w) t += s_red2[w * C + threadIdx.x];
+                for (int w = 0; w < kSmallCgWarps; ++w) t += s_red2[w * C + threadIdx.x];
                 partA[static_cast<size_t>(blockIdx.x) * bpad + ch * C + threadIdx.x] = t;
             }
             __syncthreads();
         }
         __threadfence();
         grid.sync();
-        // ---- phase 3: a = rs / pq, r -= a*q, r.r partials
+        // ---- phase 2: a = rs / pq, r -= a*q, r.r partials
         reduce_cols(partA, s_a);  // s_a := pq
-#ifdef KZ_SMALL_DEBUG
-        if (blockIdx.x == 0 && threadIdx.x == 0)
-            printf("it %lld pq0 %g rs0 %g act0 %d grid %d nw %d total %lld\n", (long long)it, s_a[0], s_rs[0], s_act[0],
-                   (int)gridDim.x, nw, (long long)total);
-#endif
         if (threadIdx.x == 0) s_err = 0;
         __syncthreads();
         for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
@@ -316,7 +391,7 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         }
         __threadfence();
         grid.sync();
-        // ---- phase 4: stop test, b = rs'/rs, x += a*p, p = r + b*p
+        // ---- phase 3: stop test, b = rs'/rs, x += a*p, p = r + b*p
         reduce_cols(partB, s_b);  // s_b := r.r
         for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
             double bc = 0.0;
@@ -365,6 +440,31 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
         grid.sync();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *s.n_active = 0;
+    if (a.scores) {
+        // ---- output: clamp(x) through perm; the packed reports ----
+        __threadfence();
+        grid.sync();
+        for (int ch = 0; ch < nch; ++ch)
+            for (int64_t e = static_cast<int64_t>(e0) * C + threadIdx.x; e < static_cast<int64_t>(e1) * C;
+                 e += kSmallCgThreads) {
+                const int c = static_cast<int>(e % C), j = ch * C + c;
+                if (j >= a.b) continue;
+                const int64_t i = e / C;
+                double v = __ldcg(a.x + static_cast<size_t>(ch) * ld + e);
+                if (a.clamp) v = v > 0.0 ? v : 0.0;
+                a.scores[static_cast<size_t>(j) * a.rows + (a.perm ? a.perm[i] : i)] = v;
+            }
+        if (blockIdx.x == 0)
+            for (int j = threadIdx.x; j < a.b; j += kSmallCgThreads) {
+                kz_report rp;
+                rp.iterations = __ldcg(s.iters + j);
+                rp.converged = __ldcg(s.converged + j);
+                rp.status = __ldcg(s.status + j);
+                rp.final_residual_norm = __ldcg(s.rnorm + j);
+                rp.rhs_norm = sqrt(__ldcg(s.bnorm2 + j));
+                a.reports[j] = rp;
+            }
+    }
 }
 
 // Grid of the fused loop (at most one CTA per SM), or 0 when it does not apply.
