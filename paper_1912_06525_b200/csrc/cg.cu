@@ -119,9 +119,10 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.qpos = cv.take<int64_t>(w.bpad);
     w.iperm = cv.take<int64_t>(g->rows);
     w.y = eig ? cv.take<double>(static_cast<size_t>(w.bpad) * eig->ldr) : nullptr;
-    w.small_part = cv.take<double>(2 * static_cast<size_t>(num_sms()) * w.bpad);
-    w.small_carry = cv.take<double>(static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.bpad);
-    w.small_stamp = cv.take<int32_t>(static_cast<size_t>(num_sms()) * (kSmallCgThreads / 32) * w.nchunks);
+    const size_t small_ctas = static_cast<size_t>(num_sms()) * kSmallCgCtasPerSm;
+    w.small_part = cv.take<double>(2 * small_ctas * w.bpad);
+    w.small_carry = cv.take<double>(small_ctas * kSmallCgWarps * w.bpad);
+    w.small_stamp = cv.take<int32_t>(small_ctas * kSmallCgWarps * w.nchunks);
     w.dev_reports = cv.take<kz_report>(w.bpad);
 }
 

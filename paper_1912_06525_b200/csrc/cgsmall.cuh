@@ -8,7 +8,9 @@
 // Per iteration, exactly the reference recurrence of cg() (solver.py:78-95)
 // for every column:
 //   1  q = p - beta*A p over a merge-path share of (rows + entries) per warp
-//      (K1's pipelined row gathers with coherent L2 loads); a row split
+//      (K1's pipelined row gathers, L1-cached: the hub rows every warp
+//      gathers stay on the SM; each grid barrier is preceded by a gpu-scope
+//      fence, which invalidates L1); a row split
 //      across warps leaves its earlier parts as carries, published with a
 //      per-(warp, chunk) iteration stamp, and the warp owning the row's end
 //      adds them in warp order; p.q partials per CTA
@@ -27,6 +29,10 @@
 
 #include <cooperative_groups.h>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "blockops.cuh"
 
 namespace kz {
@@ -36,6 +42,15 @@ constexpr int kSmallCgMaxCols = 256;                   // columns (bpad) the fus
 constexpr size_t kSmallCgElems = size_t(1) << 22;      // block size (doubles) up to which it is used
 constexpr int64_t kSmallCgMaxNnz = int64_t(1) << 24;   // ... and operator entries
 constexpr int kSmallCgWarps = kSmallCgThreads / 32;
+#ifndef KZ_SMALL_CTAS
+#define KZ_SMALL_CTAS 1  // resident CTAs per SM (more: longer barriers and reductions, measured slower)
+#endif
+constexpr int kSmallCgCtasPerSm = KZ_SMALL_CTAS;
+constexpr int32_t kSmallCgWarpRow = 32;  // rows longer than this are gathered by the whole warp
+// (entries + rows) * columns up to which the fused loop is used: its 8 warps
+// per SM hide less gather latency than K1's 40, so above ~10^7 (R-MAT 16 at
+// 64 columns: 1.2e8) the host-driven loop is faster (2.8 vs ~1.5 ms)
+constexpr double kSmallCgMaxWork = 1e7;
 
 struct SmallCgArgs {
     int32_t rows, nchunks, b, bpad;
@@ -77,8 +92,26 @@ __device__ __forceinline__ int warp_of(int64_t pos, int64_t total, int nw) {
     return w;
 }
 
+#ifdef KZ_SMALL_DEBUG
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define KZ_PT(k) \
+    if (blockIdx.x == 0 && threadIdx.x == 0) ph[k] += gtimer() - t0, t0 = gtimer();
+__device__ unsigned long long g_slowest_warp;  // (phase-1 ns << 20) | warp of the slowest warp, last iteration
+__device__ unsigned int g_wt[8192];            // per-warp phase-1 ns, last iteration
+__device__ unsigned int g_wt2[8192];           // per-warp ns until the end of the gathers (before the CTA partial)
+#else
+#define KZ_PT(k)
+#endif
+
 template <int C>
-__global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a) {
+__global__ void __launch_bounds__(kSmallCgThreads, kSmallCgCtasPerSm) cg_small_kernel(SmallCgArgs a) {
+#ifdef KZ_SMALL_DEBUG
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t0 = gtimer();
+#endif
     namespace cgr = cooperative_groups;
     cgr::grid_group grid = cgr::this_grid();
     using K = Cfg<C>;
@@ -228,6 +261,11 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
     for (;;) {
         if (!s_any || it >= s.max_iter) break;
         ++it;
+        KZ_PT(0);
+#ifdef KZ_SMALL_DEBUG
+        const unsigned long long w_t0 = gtimer();
+        if (gw == 0 && lane == 0) g_slowest_warp = 0;
+#endif
         // ---- phase 1: q = p - beta*A p over the merge-path share, p.q partials.
         // Rows wholly inside the share run one per lane group (K1's short-row
         // gather: R neighbours in flight, next indices prefetched); the split
@@ -244,7 +282,7 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
                 const int32_t in1 = row_endpos(rs1) < E ? rs1 : rs1 - 1;
                 auto finish = [&](int32_t i, const double (&acc)[VEC]) {  // q_i and its p.q term
                     double pv[VEC], qv[VEC];
-                    ld_cg_vec<VEC>(pc + static_cast<size_t>(i) * C + lg * VEC, pv);
+                    ld_plain<VEC>(pc + static_cast<size_t>(i) * C + lg * VEC, pv);
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) {
                         qv[v] = __dadd_rn(pv[v], __dmul_rn(-a.beta, acc[v]));
@@ -252,15 +290,7 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
                     }
                     st_plain<VEC>(qc + static_cast<size_t>(i) * C + lg * VEC, qv);
                 };
-                for (int32_t i = in0 + grp; i <= in1; i += K::NGW) {
-                    double acc[VEC];
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-                    gather_rows<C, false, true>(a.colidx, a.rowptr[i], a.rowptr[i + 1], K::R, pc, lg, gbase, gmask,
-                                                acc);
-                    finish(i, acc);
-                }
-                // whole-warp piece of a split row, summed over the lane groups
+                // whole-warp gather of entries [beg, end), summed over the lane groups
                 auto piece = [&](int32_t beg, int32_t end, double (&acc)[VEC]) {
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
@@ -271,6 +301,75 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
 #pragma unroll
                         for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
                 };
+                // rows inside the share: long ones across the whole warp (one
+                // lane group would take deg/R dependent rounds), short ones one
+                // per lane group
+                for (int32_t i = in0; i <= in1; ++i) {
+                    if (a.rowptr[i + 1] - a.rowptr[i] <= kSmallCgWarpRow) continue;
+                    double acc[VEC];
+                    piece(a.rowptr[i], a.rowptr[i + 1], acc);
+                    if (grp == 0) finish(i, acc);
+                }
+                // one lane group per row.  Rows of at most SR entries take one
+                // gather round each; a group works on U of them at once (all
+                // their row bounds, indices, gathers and p loads in flight
+                // together -- the latency chain of a short row is rowptr ->
+                // index -> gather, and this kernel has only 8 warps per SM to
+                // hide it).  Longer rows (<= kSmallCgWarpRow) use K1's
+                // pipelined gather.
+                constexpr int SR = K::R < K::G ? K::R : K::G;  // entries one round covers
+                constexpr int U = 4;
+                for (int32_t i0 = in0 + grp; i0 <= in1; i0 += U * K::NGW) {
+                    int32_t beg[U], deg[U], idx[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int32_t i = i0 + u * K::NGW;
+                        beg[u] = i <= in1 ? __ldg(a.rowptr + i) : 0;
+                        deg[u] = i <= in1 ? __ldg(a.rowptr + i + 1) - beg[u] : 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) idx[u] = (deg[u] <= SR && lg < deg[u]) ? __ldg(a.colidx + beg[u] + lg) : 0;
+                    double pv[U][VEC], vv[U][SR][VEC];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int32_t i = i0 + u * K::NGW;
+                        if (deg[u] <= SR && i <= in1) {
+                            ld_plain<VEC>(pc + static_cast<size_t>(i) * C + lg * VEC, pv[u]);
+#pragma unroll
+                            for (int t = 0; t < SR; ++t) {
+                                const int32_t j = __shfl_sync(gmask, idx[u], gbase + t);
+                                if (t < deg[u]) ld_plain<VEC>(pc + static_cast<size_t>(j) * C + lg * VEC, vv[u][t]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int32_t i = i0 + u * K::NGW;
+                        if (i > in1 || deg[u] > kSmallCgWarpRow) continue;
+                        double acc[VEC];
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+                        if (deg[u] <= SR) {
+#pragma unroll
+                            for (int t = 0; t < SR; ++t)
+                                if (t < deg[u]) {
+#pragma unroll
+                                    for (int v = 0; v < VEC; ++v) acc[v] += vv[u][t][v];
+                                }
+                            double qv[VEC];
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) {
+                                qv[v] = __dadd_rn(pv[u][v], __dmul_rn(-a.beta, acc[v]));
+                                dot[v] = fma(pv[u][v], qv[v], dot[v]);
+                            }
+                            st_plain<VEC>(qc + static_cast<size_t>(i) * C + lg * VEC, qv);
+                        } else {
+                            gather_rows<C, false, true>(a.colidx, beg[u], beg[u] + deg[u], K::R, pc, lg, gbase, gmask,
+                                                        acc);
+                            finish(i, acc);
+                        }
+                    }
+                }
                 auto publish = [&](const double (&acc)[VEC]) {  // carry_last + stamp
                     if (grp == 0) st_plain<VEC>(carry_last + static_cast<size_t>(gw) * bpad + ch * C + lg * VEC, acc);
                     __threadfence();
@@ -297,35 +396,46 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
                     publish(acc);
                 }
                 if (first_split) {
-                    // the earlier parts of row rs0 (warps w0 .. gw-1), in warp order;
-                    // every warp publishes before it waits, so this cannot deadlock
+                    // the earlier parts of row rs0 (warps w0 .. gw-1): every lane
+                    // waits for the stamps of its warps in parallel, then lane
+                    // group g sums warps w0+g, w0+g+NGW, ... and a fixed
+                    // butterfly over the groups combines them.  Every warp
+                    // publishes before it waits, so this cannot deadlock.
+                    for (int w = w0 + lane; w < gw; w += 32) {
+                        if (total * (w + 1) / nw <= total * w / nw) continue;  // an empty share holds no part
+                        volatile int32_t* f = a.stamp + static_cast<size_t>(w) * nch + ch;
+#if KZ_CHECKED
+                        long long spins = 0;
+                        while (*f != static_cast<int32_t>(it)) KZ_DCHECK(++spins < (1ll << 28));
+#else
+                        while (*f != static_cast<int32_t>(it)) {
+                        }
+#endif
+                    }
+                    __syncwarp();
+                    __threadfence();
                     double acc[VEC];
 #pragma unroll
                     for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-                    for (int w = w0; w < gw; ++w) {
-                        if (total * (w + 1) / nw <= total * w / nw) continue;  // an empty share holds no part
-                        if (lane == 0) {
-                            volatile int32_t* f = a.stamp + static_cast<size_t>(w) * nch + ch;
-#if KZ_CHECKED
-                            long long spins = 0;
-                            while (*f != static_cast<int32_t>(it)) KZ_DCHECK(++spins < (1ll << 28));
-#else
-                            while (*f != static_cast<int32_t>(it)) {
-                            }
-#endif
-                        }
-                        __syncwarp();
-                        __threadfence();
+                    for (int w = w0 + grp; w < gw; w += K::NGW) {
+                        if (total * (w + 1) / nw <= total * w / nw) continue;
                         double t[VEC];
                         ld_cg_vec<VEC>(carry_last + static_cast<size_t>(w) * bpad + ch * C + lg * VEC, t);
 #pragma unroll
                         for (int v = 0; v < VEC; ++v) acc[v] += t[v];
                     }
 #pragma unroll
+                    for (int off = K::G; off < 32; off <<= 1)
+#pragma unroll
+                        for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+#pragma unroll
                     for (int v = 0; v < VEC; ++v) acc[v] += tail[v];
                     if (grp == 0) finish(rs0, acc);
                 }
             }
+#ifdef KZ_SMALL_DEBUG
+            if (lane == 0 && gw < 8192) g_wt2[gw] = static_cast<unsigned int>(gtimer() - w_t0);
+#endif
             // warp p.q partial (butterfly over the lane groups) -> CTA partial, warps in order
 #pragma unroll
             for (int off = K::G; off < 32; off <<= 1)
@@ -343,8 +453,14 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
             }
             __syncthreads();
         }
+        KZ_PT(1);
+#ifdef KZ_SMALL_DEBUG
+        if (lane == 0) atomicMax(&g_slowest_warp, ((gtimer() - w_t0) << 20) | static_cast<unsigned long long>(gw));
+        if (lane == 0 && gw < 8192) g_wt[gw] = static_cast<unsigned int>(gtimer() - w_t0);
+#endif
         __threadfence();
         grid.sync();
+        KZ_PT(2);
         // ---- phase 2: a = rs / pq, r -= a*q, r.r partials
         reduce_cols(partA, s_a);  // s_a := pq
         if (threadIdx.x == 0) s_err = 0;
@@ -389,8 +505,10 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
             }
             cta_partial(rr, ch, partB);
         }
+        KZ_PT(3);
         __threadfence();
         grid.sync();
+        KZ_PT(4);
         // ---- phase 3: stop test, b = rs'/rs, x += a*p, p = r + b*p
         reduce_cols(partB, s_b);  // s_b := r.r
         for (int c = threadIdx.x; c < bpad; c += kSmallCgThreads) {
@@ -436,9 +554,33 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
             }
         }
         chunk_flags();
+        KZ_PT(5);
         __threadfence();
         grid.sync();
+        KZ_PT(6);
     }
+#ifdef KZ_SMALL_DEBUG
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long sw = g_slowest_warp;
+        const int w = static_cast<int>(sw & 0xfffff);
+        const int64_t Sw = total * w / nw, Ew = total * (w + 1) / nw;
+        const int32_t r0w = merge_row(a.rowptr, a.rows, Sw), r1w = merge_row(a.rowptr, a.rows, Ew - 1);
+        printf("slowest warp %d: %.2f us, rows %d..%d (deg %d .. %d), split start %d\n", w, (sw >> 20) / 1e3, r0w, r1w,
+               a.rowptr[r0w + 1] - a.rowptr[r0w], a.rowptr[r1w + 1] - a.rowptr[r1w],
+               (int)(static_cast<int64_t>(a.rowptr[r0w]) + r0w < Sw));
+        for (int ww = 0; ww < nw && ww < 8192; ++ww) {
+            if (g_wt[ww] < 10000) continue;  // only the slow ones (> 10 us)
+            const int64_t S2 = total * ww / nw, E2 = total * (ww + 1) / nw;
+            const int32_t a0 = merge_row(a.rowptr, a.rows, S2), a1 = merge_row(a.rowptr, a.rows, E2 - 1);
+            printf("  warp %d: gathers %.2f us, phase %.2f us, rows %d..%d degs %d %d inner %d\n", ww, g_wt2[ww] / 1e3,
+                   g_wt[ww] / 1e3, a0, a1, a.rowptr[a0 + 1] - a.rowptr[a0], a.rowptr[a1 + 1] - a.rowptr[a1], a1 - a0 + 1);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("small cg: %lld it, us per it: top %.2f ph1 %.2f sync %.2f ph2 %.2f sync %.2f ph3 %.2f sync %.2f\n",
+               (long long)it, ph[0] / 1e3 / it, ph[1] / 1e3 / it, ph[2] / 1e3 / it, ph[3] / 1e3 / it, ph[4] / 1e3 / it,
+               ph[5] / 1e3 / it, ph[6] / 1e3 / it);
+#endif
     if (blockIdx.x == 0 && threadIdx.x == 0) *s.n_active = 0;
     if (a.scores) {
         // ---- output: clamp(x) through perm; the packed reports ----
@@ -470,16 +612,32 @@ __global__ void __launch_bounds__(kSmallCgThreads) cg_small_kernel(SmallCgArgs a
 // Grid of the fused loop (at most one CTA per SM), or 0 when it does not apply.
 inline int small_cg_grid(int64_t rows, int64_t nnz, int C, int bpad, const void* kernel) {
     if (bpad > kSmallCgMaxCols || (kSmallCgThreads % C) != 0 || nnz > kSmallCgMaxNnz ||
-        static_cast<size_t>(rows) * bpad > kSmallCgElems)
+        static_cast<size_t>(rows) * bpad > kSmallCgElems ||
+        static_cast<double>(nnz + rows) * bpad > kSmallCgMaxWork)
         return 0;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSmallCgThreads, 0) != cudaSuccess ||
-        per_sm < 1) {
-        cudaGetLastError();
-        return 0;
+    // occupancy of each kernel instantiation, queried once per device
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> occ;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = -1;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (const auto& e : occ)
+            if (e.first.first == kernel && e.first.second == dev) per_sm = e.second;
+        if (per_sm < 0) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSmallCgThreads, 0) != cudaSuccess) {
+                cudaGetLastError();
+                per_sm = 0;
+            }
+            occ.push_back({{kernel, dev}, per_sm});
+        }
     }
-    const int64_t want = std::max<int64_t>(1, (nnz + rows) / 512);
-    return static_cast<int>(std::min<int64_t>(num_sms(), want));
+    if (per_sm < 1) return 0;
+    // gathers are latency-bound: as many resident warps as the registers
+    // allow (the merge-path shares stay >= ~16 items per warp)
+    const int64_t want = std::max<int64_t>(1, (nnz + rows) / (16 * kSmallCgWarps));
+    return static_cast<int>(std::min<int64_t>(static_cast<int64_t>(num_sms()) * std::min(per_sm, kSmallCgCtasPerSm), want));
 }
 
 }  // namespace kz

@@ -214,9 +214,7 @@ __device__ __forceinline__ void st_stream(double* p, const double (&v)[VEC]) {
 // Sum Xg rows of neighbours col[beg..end) into acc, R neighbours per round,
 // rounds `stride` apart.  All lanes of a group share the neighbour; lane lg
 // owns columns lg*VEC .. lg*VEC+VEC-1 of the chunk.  W: weighted operator.
-// coherent (L2) gather for kernels that also write the gathered block
-// within the same launch (the fused small CG loop): .cg loads never return a
-// stale L1 / non-coherent-cache copy across its grid barriers
+// .cg (L2-only) loads of data other CTAs wrote in the same launch
 template <int VEC>
 __device__ __forceinline__ void ld_cg_vec(const double* p, double (&v)[VEC]) {
     if constexpr (VEC == 4) {
@@ -232,6 +230,9 @@ __device__ __forceinline__ void ld_cg_vec(const double* p, double (&v)[VEC]) {
     }
 }
 
+// CO: the gathered block is written within the same launch (the fused small
+// CG loop): coherent L1-cached loads instead of the non-coherent path; the
+// kernel's gpu-scope fences before each grid barrier invalidate L1 (CCTL.IVALL)
 template <int C, bool W = false, bool CO = false>
 __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int beg, int end,
                                             int stride, const double* __restrict__ Xc, int lg,
@@ -288,7 +289,7 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
                 ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #else
             if constexpr (CO)
-                ld_cg_vec<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
+                ld_plain<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
             else
                 ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #endif

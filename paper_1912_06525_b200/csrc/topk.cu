@@ -322,6 +322,8 @@ __global__ void __launch_bounds__(kSmallThreads)
     __shared__ int s_bin, s_cum;
     const int j = blockIdx.x;
     const double* col = scores + static_cast<size_t>(j) * n;
+    int scap = 64;
+    while (scap < 2 * k && scap < kCap) scap <<= 1;
     if (threadIdx.x == 0) {
         c = ColState{};
         c.shift = 96;
@@ -333,11 +335,23 @@ __global__ void __launch_bounds__(kSmallThreads)
         __syncthreads();
         const ColState cc = c;
         const int ns = max(cc.shift - kDigit, 0);
-        for (int64_t i = threadIdx.x; i < n; i += kSmallThreads) {
-            const unsigned long long hi = score_key(col[i]);
-            const unsigned int lo = ~static_cast<unsigned int>(i);
-            if (cmp_prefix(hi, lo, cc, cc.shift) == 0 && !above_bound(m, j, hi, lo))
-                atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
+        // 4 loads in flight per thread (the scan is latency-bound at these sizes)
+        for (int64_t i0 = threadIdx.x; i0 < n; i0 += 4 * kSmallThreads) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t i = i0 + u * kSmallThreads;
+                v[u] = i < n ? col[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t i = i0 + u * kSmallThreads;
+                if (i >= n) break;
+                const unsigned long long hi = score_key(v[u]);
+                const unsigned int lo = ~static_cast<unsigned int>(i);
+                if (cmp_prefix(hi, lo, cc, cc.shift) == 0 && !above_bound(m, j, hi, lo))
+                    atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
+            }
         }
         __syncthreads();
         // masked ids leave the histogram (topk_mask_kernel)
@@ -395,7 +409,9 @@ __global__ void __launch_bounds__(kSmallThreads)
                     c.phi |= v >> 32;
                 }
                 c.shift = ns;
-                if (c.above + static_cast<int>(pivot) <= kCap || ns == 0) c.done = 1;
+                // refine until few candidates remain: the final sort is the
+                // costly step here (bitonic over the next power of two)
+                if (c.above + static_cast<int>(pivot) <= scap || ns == 0) c.done = 1;
             }
         }
         __syncthreads();
@@ -404,14 +420,25 @@ __global__ void __launch_bounds__(kSmallThreads)
     if (threadIdx.x == 0) c.ncand = 0;
     __syncthreads();
     const ColState cc = c;
-    for (int64_t i = threadIdx.x; i < n; i += kSmallThreads) {
-        const unsigned long long hi = score_key(col[i]);
-        const unsigned int lo = ~static_cast<unsigned int>(i);
-        if (cmp_prefix(hi, lo, cc, cc.shift) >= 0 && !above_bound(m, j, hi, lo) && !is_masked(m, j, i)) {
-            const int pos = atomicAdd(&c.ncand, 1);
-            if (pos < kCap) {
-                sk[pos] = hi;
-                si[pos] = static_cast<int>(i);
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += 4 * kSmallThreads) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * kSmallThreads;
+            v[u] = i < n ? col[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * kSmallThreads;
+            if (i >= n) break;
+            const unsigned long long hi = score_key(v[u]);
+            const unsigned int lo = ~static_cast<unsigned int>(i);
+            if (cmp_prefix(hi, lo, cc, cc.shift) >= 0 && !above_bound(m, j, hi, lo) && !is_masked(m, j, i)) {
+                const int pos = atomicAdd(&c.ncand, 1);
+                if (pos < kCap) {
+                    sk[pos] = hi;
+                    si[pos] = static_cast<int>(i);
+                }
             }
         }
     }

@@ -21,3 +21,26 @@ int main() {
         printf("grid %d: %s, %.2f us per grid.sync\n", grid, cudaGetErrorString(e), ms * 1000 / iters);
     }
 }
+// (appended) host-side cost of a cooperative launch vs a plain launch
+#include <chrono>
+__global__ void empty_k(int* a) { if (a && threadIdx.x == 1023) a[0] = 1; }
+struct CoopTimer {
+    CoopTimer() {
+        int* a = nullptr;
+        void* args[] = {&a};
+        cudaStream_t st;
+        cudaStreamCreate(&st);
+        for (int w = 0; w < 2; ++w) {
+            auto t0 = std::chrono::high_resolution_clock::now();
+            for (int i = 0; i < 200; ++i) cudaLaunchCooperativeKernel((void*)empty_k, 148, 256, args, 0, st);
+            cudaStreamSynchronize(st);
+            auto t1 = std::chrono::high_resolution_clock::now();
+            for (int i = 0; i < 200; ++i) empty_k<<<148, 256, 0, st>>>(a);
+            cudaStreamSynchronize(st);
+            auto t2 = std::chrono::high_resolution_clock::now();
+            if (w) printf("cooperative launch %.2f us, plain launch %.2f us (host+device, 200 back to back)\n",
+                          std::chrono::duration<double, std::micro>(t1 - t0).count() / 200,
+                          std::chrono::duration<double, std::micro>(t2 - t1).count() / 200);
+        }
+    }
+} coop_timer_instance;
