@@ -93,6 +93,9 @@ enum TaskType : int { TASK_S = 0, TASK_M = 1, TASK_L = 2 };
 #ifndef KZ_K1_VEC32
 #define KZ_K1_VEC32 4  // doubles per lane of a gathered row for C >= 32 (2: 16-byte, 4: 32-byte loads)
 #endif
+#ifndef KZ_K1_VEC16
+#define KZ_K1_VEC16 2  // doubles per lane of a gathered row for C = 16 (experiments: 4 = 32-byte loads)
+#endif
 #ifndef KZ_K1_SMEM_DOT
 #define KZ_K1_SMEM_DOT 1  // 1: column-dot accumulators in shared memory instead of registers
 #endif
@@ -107,7 +110,7 @@ template <int C>
 struct Cfg {
     // doubles per lane of a gathered row: 16-byte loads, or 32-byte
     // (LDG.256, sm_100) loads for wide chunks
-    static constexpr int VEC = (C >= 32) ? KZ_K1_VEC32 : (C >= 2 ? 2 : 1);
+    static constexpr int VEC = (C >= 32) ? KZ_K1_VEC32 : (C >= 16 ? KZ_K1_VEC16 : (C >= 2 ? 2 : 1));
     static constexpr int SVEC = (C >= 2) ? 2 : 1;  // doubles per lane of the streaming kernels
     static constexpr int G = C / VEC;             // lanes per row group
     static constexpr int NGW = 32 / G;            // row groups per warp
@@ -144,6 +147,26 @@ __device__ __forceinline__ void ld_nc_hint4(const double* p, double (&v)[4], uin
     asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
                  : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                  : "l"(p), "l"(pol));
+}
+#ifndef KZ_K1_L1HINT
+#define KZ_K1_L1HINT 0  // experiments: per-row L1 policy (1: hub evict_last / tail no_allocate, 2: hub evict_last / tail evict_first)
+#endif
+// gather with an L1 eviction priority chosen per row: the hottest hub rows
+// stay in L1, the tail rows pass through without displacing them
+__device__ __forceinline__ void ld_nc_l1hint4(const double* p, double (&v)[4], bool hub) {
+    if (hub) {
+        asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(p));
+    } else {
+#if KZ_K1_L1HINT == 2
+        asm volatile("ld.global.nc.L1::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+#else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+#endif
+                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                     : "l"(p));
+    }
 }
 // Predicated gather: lanes with !pred issue no memory request and read 0.
 template <int VEC>
@@ -285,6 +308,13 @@ __device__ __forceinline__ void gather_rows(const int32_t* __restrict__ col, int
 #elif KZ_K1_L2HINT
             if constexpr (K::VEC == 4)
                 ld_nc_hint4(Xl + static_cast<size_t>(j) * C, v[t], j < hub_rows ? pol_hub : pol_tail);
+            else
+                ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
+#elif KZ_K1_L1HINT
+            if constexpr (K::VEC == 4 && !CO)
+                ld_nc_l1hint4(Xl + static_cast<size_t>(j) * C, v[t], j < hub_rows);
+            else if constexpr (CO)
+                ld_plain<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
             else
                 ld_nc<K::VEC>(Xl + static_cast<size_t>(j) * C, v[t]);
 #else
@@ -441,7 +471,7 @@ template <int C, bool W>
 __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs a) {
     using K = Cfg<C>;
     constexpr int VEC = K::VEC;
-    constexpr bool SD = (KZ_K1_SMEM_DOT != 0) && C >= 32;
+    constexpr bool SD = (KZ_K1_SMEM_DOT != 0) && (C >= 32 || VEC == 4);
     __shared__ double s_dacc[SD ? VEC * kThreads : 1];
     const int lane = threadIdx.x & 31;
     const int gw = lane / K::G, lg = lane % K::G, gbase = gw * K::G;
@@ -777,7 +807,7 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
     if (a.ldd == 0) a.ldd = g->rows * C;
     a.vals = g->vals;
     const bool w = g->vals != nullptr;
-#if KZ_K1_L2HINT
+#if KZ_K1_L2HINT || KZ_K1_L1HINT
     static const int hub_rows_env = [] {
         const char* e = std::getenv("KZ_K1_HUBROWS");
         return e ? std::atoi(e) : 131072;

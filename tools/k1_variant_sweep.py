@@ -27,6 +27,7 @@ ap.add_argument("--reps", type=int, default=9)
 ap.add_argument("--tag", default="base")
 ap.add_argument("--save", action="store_true")
 ap.add_argument("--cache", default="/tmp/k1sweep")
+ap.add_argument("--chunk", type=int, default=32)
 a = ap.parse_args()
 
 os.makedirs(a.cache, exist_ok=True)
@@ -43,7 +44,7 @@ else:
     n, nnz = g.n, g.nnz
     np.savez(cf, off=off, col=col, n=n, nnz=nnz)
 
-b, C = a.b, 32
+b, C = a.b, a.chunk
 gen = torch.Generator(device="cuda").manual_seed(0)
 X = torch.randn(b * n, dtype=torch.float64, device="cuda", generator=gen)
 Y = torch.empty_like(X)
@@ -59,7 +60,7 @@ for r in range(a.reps + 2):
     torch.cuda.synchronize()
     if r >= 2:
         ts.append(e0.elapsed_time(e1))
-rf = os.path.join(a.cache, f"ref{a.scale}.pt")
+rf = os.path.join(a.cache, f"ref{a.scale}_c{C}.pt")
 if a.save:
     torch.save({"Y": Y.cpu(), "d": dots.cpu()}, rf)
     err = derr = 0.0
