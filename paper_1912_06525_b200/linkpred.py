@@ -142,6 +142,107 @@ def katz_rank(idx, q, s, tol=1e-10):
     return katz_rank_batch(idx, [q], s, tol)[0]
 
 
+class SparseKatzEngine:
+    """The three device stages of sparse_katz (linkpred.py:165-207) for a
+    batch of queries: (1) query solves, masked top-s candidates, top-T
+    anchors and the reference profiles; (2) anchor solves gathered straight
+    into candidate profiles (K7 gather); (3) the Pearson rerank (K7).
+    ``sparse_katz_batch`` runs them in one process; ``distributed.
+    sparse_katz_distributed`` runs stage 2 on the globally deduplicated anchor
+    set, sharded over the ranks."""
+
+    def __init__(self, idx, s, T=None, tol=1e-10, anchor_batch=256):
+        if s < 1:
+            raise ValueError("s must be >= 1")
+        if T is None:
+            T = s + 1
+        if T < 1:
+            raise ValueError("need at least one anchor")
+        if T > idx.n - 1:
+            raise ValueError(f"T={T} anchors not available on {idx.n} nodes")
+        self.idx, self.T, self.tol, self.anchor_batch = idx, int(T), tol, int(anchor_batch)
+        self.s_eff = min(int(s), idx.n)
+        self.torch = _lib.torch_cuda()
+
+    def query_stage(self, qs):
+        """-> dict(qs, top [b][s] int64, top_vals, counts [b] int32, anc [b][T]
+        int64, ref [b][T+1], profiles [b][T+1][s] with row 0 filled); device
+        tensors, ids internal."""
+        torch, idx, T = self.torch, self.idx, self.T
+        qs = np.atleast_1d(np.asarray(qs, dtype=np.int64))
+        try:
+            scores, internal = _query_batch_state(idx, qs, self.tol)
+        except KeyError as err:
+            raise solver.UnknownNodeError(str(err)) from None
+        b = scores.shape[0]
+        top, top_vals, counts = topk_device(scores, self.s_eff, idx.mask_operator(), internal, internal)
+        anc, _, _ = topk_device(scores, T, None, None, internal)
+        # reference profile [K(q,q), K(a_i,q)]  (linkpred.py:189-191)
+        qidx = torch.as_tensor(internal, dtype=torch.int64, device="cuda")
+        rows = torch.arange(b, device="cuda")
+        ref = torch.empty((b, T + 1), dtype=torch.float64, device="cuda")
+        ref[:, 0] = scores[rows, qidx]
+        ref[:, 1:] = torch.gather(scores, 1, anc)
+        profiles = torch.empty((b, T + 1, self.s_eff), dtype=torch.float64, device="cuda")
+        profiles[:, 0, :] = top_vals
+        return {"qs": qs, "top": top, "top_vals": top_vals, "counts": counts, "anc": anc, "ref": ref,
+                "profiles": profiles}
+
+    def anchor_stage(self, uniq, inverse, u0, top, counts, profiles):
+        """Solve the anchors uniq (internal ids) in batches and write
+        profiles[j][i+1][:] = K(anchor, top[j][:]) for every slot (j, i) with
+        u0 <= inverse[j][i] < u0 + len(uniq); inverse indexes the global
+        unique list whose slice [u0, u0+len(uniq)) is `uniq`."""
+        torch, idx = self.torch, self.idx
+        lib = _lib.load()
+        st = _lib.stream_ptr(torch)
+        n = idx.n
+        T1 = profiles.shape[1]
+        for s0 in range(0, len(uniq), self.anchor_batch):
+            chunk = uniq[s0 : s0 + self.anchor_batch]
+            a_scores, _ = solver.query_batch(idx, idx.id_map[chunk], tol=self.tol, device=True)
+            lo = u0 + s0
+            sel = np.argwhere((inverse >= lo) & (inverse < lo + chunk.size))
+            trip = np.stack([inverse[sel[:, 0], sel[:, 1]] - lo, sel[:, 0], sel[:, 1] + 1], axis=1)
+            trip_d = torch.as_tensor(np.ascontiguousarray(trip, dtype=np.int64), device="cuda")
+            _lib.check(lib.kz_profile_gather(_lib.ptr(a_scores), n, int(trip.shape[0]), _lib.ptr(trip_d),
+                                             _lib.ptr(top), _lib.ptr(counts), self.s_eff, _lib.ptr(profiles),
+                                             T1, st))
+            del a_scores
+
+    def rerank_stage(self, state):
+        """Pearson rerank of every query's candidates -> [RankedPrediction]."""
+        torch, idx, s_eff = self.torch, self.idx, self.s_eff
+        lib = _lib.load()
+        st = _lib.stream_ptr(torch)
+        top, top_vals, counts = state["top"], state["top_vals"], state["counts"]
+        profiles, ref = state["profiles"], state["ref"]
+        b, T1 = ref.shape
+        corr = torch.empty((b, s_eff), dtype=torch.float64, device="cuda")
+        big = s_eff > _RERANK_SMEM
+        order = None if big else torch.empty((b, s_eff), dtype=torch.int64, device="cuda")
+        _lib.check(lib.kz_pearson_rerank(_lib.ptr(profiles), _lib.ptr(ref), _lib.ptr(top), _lib.ptr(top_vals),
+                                         _lib.ptr(counts), b, T1, s_eff, _lib.ptr(corr), _lib.ptr(order), st))
+        if big:
+            # more candidates than one CTA sorts in shared memory: the same
+            # lexsort((top, -score, -corr)) as three stable device sorts
+            valid = torch.arange(s_eff, device="cuda").unsqueeze(0) < counts.unsqueeze(1)
+            key_c = torch.where(valid, -corr, torch.full_like(corr, float("inf")))
+            order = torch.argsort(top, dim=1, stable=True)
+            order = torch.gather(order, 1, torch.argsort(torch.gather(-top_vals, 1, order), dim=1, stable=True))
+            order = torch.gather(order, 1, torch.argsort(torch.gather(key_c, 1, order), dim=1, stable=True))
+        top_h, corr_h, order_h, counts_h = (top.cpu().numpy(), corr.cpu().numpy(), order.cpu().numpy(),
+                                            counts.cpu().numpy())
+        out = []
+        for j, q in enumerate(state["qs"].tolist()):
+            m = int(counts_h[j])
+            o = order_h[j, :m]
+            ids_j = np.asarray(idx.id_map)[top_h[j, o]]
+            cands = list(zip(ids_j.tolist(), corr_h[j, o].tolist()))
+            out.append(RankedPrediction(query=q, candidates=cands, method="sparse-katz"))
+        return out
+
+
 def sparse_katz_batch(idx, qs, s, T=None, tol=1e-10, anchor_batch=256):
     """sparse_katz for many queries (linkpred.py:165-207), batched.
 
@@ -149,72 +250,12 @@ def sparse_katz_batch(idx, qs, s, T=None, tol=1e-10, anchor_batch=256):
     ``anchor_batch`` columns; each batch's scores are gathered straight into
     the candidates' profiles (K7 gather) and dropped, so the device holds at
     most one batch of anchor score vectors."""
-    if s < 1:
-        raise ValueError("s must be >= 1")
-    if T is None:
-        T = s + 1
-    if T < 1:
-        raise ValueError("need at least one anchor")
-    if T > idx.n - 1:
-        raise ValueError(f"T={T} anchors not available on {idx.n} nodes")
-    torch = _lib.torch_cuda()
-    lib = _lib.load()
-    st = _lib.stream_ptr(torch)
-    qs = np.atleast_1d(np.asarray(qs, dtype=np.int64))
-    try:
-        scores, internal = _query_batch_state(idx, qs, tol)
-    except KeyError as err:
-        raise solver.UnknownNodeError(str(err)) from None
-    b, n = scores.shape
-    s_eff = min(int(s), n)
-    top, top_vals, counts = topk_device(scores, s_eff, idx.mask_operator(), internal, internal)
-    anc, _, anc_counts = topk_device(scores, T, None, None, internal)
-    T1 = T + 1
-    # reference profile [K(q,q), K(a_i,q)]  (linkpred.py:189-191)
-    qidx = torch.as_tensor(internal, dtype=torch.int64, device="cuda")
-    rows = torch.arange(b, device="cuda")
-    ref = torch.empty((b, T1), dtype=torch.float64, device="cuda")
-    ref[:, 0] = scores[rows, qidx]
-    ref[:, 1:] = torch.gather(scores, 1, anc)
-    profiles = torch.empty((b, T1, s_eff), dtype=torch.float64, device="cuda")
-    profiles[:, 0, :] = top_vals
-    del scores
-    anc_host = anc.cpu().numpy()
-    uniq, inverse = np.unique(anc_host, return_inverse=True)
-    inverse = inverse.reshape(b, T)
-    for s0 in range(0, uniq.size, anchor_batch):
-        chunk = uniq[s0 : s0 + anchor_batch]
-        a_scores, _ = solver.query_batch(idx, idx.id_map[chunk], tol=tol, device=True)
-        sel = np.argwhere((inverse >= s0) & (inverse < s0 + chunk.size))
-        trip = np.stack([inverse[sel[:, 0], sel[:, 1]] - s0, sel[:, 0], sel[:, 1] + 1], axis=1)
-        trip_d = torch.as_tensor(np.ascontiguousarray(trip, dtype=np.int64), device="cuda")
-        _lib.check(lib.kz_profile_gather(_lib.ptr(a_scores), n, int(trip.shape[0]), _lib.ptr(trip_d),
-                                         _lib.ptr(top), _lib.ptr(counts), s_eff, _lib.ptr(profiles),
-                                         T1, st))
-        del a_scores
-    corr = torch.empty((b, s_eff), dtype=torch.float64, device="cuda")
-    big = s_eff > _RERANK_SMEM
-    order = None if big else torch.empty((b, s_eff), dtype=torch.int64, device="cuda")
-    _lib.check(lib.kz_pearson_rerank(_lib.ptr(profiles), _lib.ptr(ref), _lib.ptr(top), _lib.ptr(top_vals),
-                                     _lib.ptr(counts), b, T1, s_eff, _lib.ptr(corr), _lib.ptr(order), st))
-    if big:
-        # more candidates than one CTA sorts in shared memory: the same
-        # lexsort((top, -score, -corr)) as three stable device sorts
-        valid = torch.arange(s_eff, device="cuda").unsqueeze(0) < counts.unsqueeze(1)
-        key_c = torch.where(valid, -corr, torch.full_like(corr, float("inf")))
-        order = torch.argsort(top, dim=1, stable=True)
-        order = torch.gather(order, 1, torch.argsort(torch.gather(-top_vals, 1, order), dim=1, stable=True))
-        order = torch.gather(order, 1, torch.argsort(torch.gather(key_c, 1, order), dim=1, stable=True))
-    top_h, corr_h, order_h, counts_h = (top.cpu().numpy(), corr.cpu().numpy(), order.cpu().numpy(),
-                                        counts.cpu().numpy())
-    out = []
-    for j, q in enumerate(qs.tolist()):
-        m = int(counts_h[j])
-        o = order_h[j, :m]
-        ids_j = np.asarray(idx.id_map)[top_h[j, o]]
-        cands = list(zip(ids_j.tolist(), corr_h[j, o].tolist()))
-        out.append(RankedPrediction(query=q, candidates=cands, method="sparse-katz"))
-    return out
+    eng = SparseKatzEngine(idx, s, T, tol, anchor_batch)
+    state = eng.query_stage(qs)
+    b = state["anc"].shape[0]
+    uniq, inverse = np.unique(state["anc"].cpu().numpy(), return_inverse=True)
+    eng.anchor_stage(uniq, inverse.reshape(b, eng.T), 0, state["top"], state["counts"], state["profiles"])
+    return eng.rerank_stage(state)
 
 
 def sparse_katz(idx, q, s, T=None, tol=1e-10):

@@ -433,6 +433,21 @@ def test_sparse_katz_rerank_device_sort_fallback(torch, kz, monkeypatch):
     assert got == want
 
 
+def test_sparse_katz_distributed_single_rank_equals_batch(torch, kz):
+    """The staged path of sparse_katz_distributed (query stage, anchor stage
+    over the globally deduplicated anchors, rerank stage) on one rank gives
+    sparse_katz_batch's lists; the world-2 exchange is covered on gloo
+    (tests/test_distributed.py)."""
+    from paper_1912_06525_b200.distributed import sparse_katz_distributed
+    from paper_1912_06525_b200.linkpred import SparseKatzEngine
+
+    idx = kz.load_index(os.path.join(GOLDEN, "ba300.klrc"))
+    qs = idx.id_map[::13][:10]
+    want = [p.candidates for p in kz.sparse_katz_batch(idx, qs, 12)]
+    got = [p.candidates for p in sparse_katz_distributed(idx, qs, 12, engine=SparseKatzEngine(idx, 12))]
+    assert got == want
+
+
 def test_vec_op_rounds_like_numpy(torch, kz):
     """kz_vec_op (the generic cg() updates) rounds the products and the sum
     separately, as numpy's x += a*p, r -= a*q, p = r + b*p do."""
