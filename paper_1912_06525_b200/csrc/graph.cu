@@ -9,6 +9,12 @@
 #include <vector>
 
 #include "spmm.cuh"
+#ifndef KZ_EXPERIMENTS
+#define KZ_EXPERIMENTS 0  // 1: build the experiment entry points (tools/k1_coldpass_proto.py)
+#endif
+#if KZ_EXPERIMENTS
+#include "spmmcold.cuh"
+#endif
 
 namespace kz {
 
@@ -512,3 +518,38 @@ extern "C" int kz_spmm(const kz_graph* g, int32_t b, int32_t chunk, const double
     a.hook.dots_out = dots;
     return launch_spmm(g, chunk, nchunks, a, st);
 }
+
+#if KZ_EXPERIMENTS
+// Experiment entry (tools/k1_coldpass_proto.py): one launch of the cold pass
+// on caller-built streams (all device pointers); P[chunk][ng*slots][32].
+extern "C" int kz_spmm_cold_debug(const uint32_t* ent, const int32_t* segoff, const uint8_t* nslot,
+                                  int32_t ng, int32_t nslabs, int64_t cols, int32_t b, const double* X,
+                                  double* P, int32_t* done, void* stream) {
+    clear_error();
+    if (!ent || !segoff || !nslot || !X || !P || !done || ng < 1 || ng % (kThreads / 8) != 0 || b % 32 != 0)
+        return fail(KZ_EARG, "bad cold-pass arguments");
+    const int grid = ng / (kThreads / 8);
+    if (grid > num_sms() * cold_ctas_per_sm()) return fail(KZ_EARG, "cold-pass grid is not co-resident");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    KZ_CUDA(cudaMemsetAsync(done, 0, sizeof(int32_t) * (b / 32) * nslabs, st));
+    ColdArgs a{};
+    a.ent = ent;
+    a.segoff = segoff;
+    a.nslot = nslot;
+    a.ng = ng;
+    a.nslabs = nslabs;
+    a.nchunks = b / 32;
+    a.cols = static_cast<int32_t>(cols);
+    a.Xg = X;
+    a.ldxg = cols * 32;
+    a.P = P;
+    a.done = done;
+    {
+        const char* e = std::getenv("KZ_COLD_THROTTLE");
+        a.throttle = e ? std::atoi(e) : 1;
+    }
+    return launch_spmm_cold(a, grid, st);
+}
+
+extern "C" int kz_cold_slots(void) { return kColdSlots; }
+#endif  // KZ_EXPERIMENTS
