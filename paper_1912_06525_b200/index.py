@@ -291,8 +291,8 @@ class GraphIndex(_DeviceGraphMixin):
 
     ``reorder`` relabels the nodes *inside the solve* for gather locality
     ("degclass": degree classes, reverse Cuthill-McKee inside each; "rcm";
-    "degree"; "auto" = "degclass" for operators above 10^6 stored entries).  It is invisible at the API: right-hand sides, start vectors
-    and scores stay in internal order (the output kernel scatters back); only
+    "degree"; "auto" = ``auto_order``).  It is invisible at the API:
+    right-hand sides, start vectors and scores stay in internal order (the output kernel scatters back); only
     summation order, i.e. roundoff, changes.
     """
 
@@ -307,9 +307,10 @@ class GraphIndex(_DeviceGraphMixin):
         self.id_map = self.graph.original_ids
         g = self.graph
         mode = self.reorder
-        if mode == "auto":
-            mode = "degclass" if g.nnz > 1_000_000 else None
         self._order = None
+        if mode == "auto":
+            self._order = auto_order(g)
+            mode = None
         if mode == "rcm":
             self._order = rcm_order(g)
         elif mode == "degclass":
@@ -394,6 +395,32 @@ def degclass_rcm_order(g):
     pos[rcm] = np.arange(g.n)
     cls = -np.floor(np.log2(np.maximum(np.diff(g.row_offsets), 1))).astype(np.int64)
     return np.lexsort((pos, cls)).astype(np.int64)
+
+
+def auto_order(g):
+    """Solve order for GraphIndex(reorder="auto"), or None to keep the given
+    one.  Operators of at most 10^6 stored entries fit L2 and stay as they are.
+    Power-law graphs (max degree above 16x the mean: R-MAT, Chung-Lu) get the
+    degree-class order, which keeps the hub rows of X together in L2.  Graphs
+    without hubs (the planted-partition graph of BASELINE config 5) gain
+    nothing from degree classes; they keep the given order unless RCM brings
+    neighbours closer, measured by the median |row - col| over the stored
+    entries (SBM 10^6: the generator's community-contiguous ids give 6.06 ms
+    per CG iteration at 256 columns, RCM 6.65, degree classes 6.76;
+    tools/cfg5_order_experiment.py)."""
+    if g.nnz <= 1_000_000:
+        return None
+    deg = np.diff(g.row_offsets)
+    if deg.max() > 16.0 * deg.mean():
+        return degclass_rcm_order(g)
+    rows = np.repeat(np.arange(g.n, dtype=np.int64), deg)
+    cols = np.asarray(g.col_indices, dtype=np.int64)
+    rcm = rcm_order(g)
+    pos = np.empty(g.n, dtype=np.int64)
+    pos[rcm] = np.arange(g.n)
+    gap_given = np.median(np.abs(rows - cols))
+    gap_rcm = np.median(np.abs(pos[rows] - pos[cols]))
+    return None if gap_given <= gap_rcm else rcm
 
 
 def permute_csr(offsets, cols, order, inv):
