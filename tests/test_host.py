@@ -215,3 +215,26 @@ def test_q_recurrence_equals_reference_cg(bf):
             x, it = _q_recurrence_cg(lambda v: v - beta * (a @ v), rhs, 1e-8)
             assert it == rep.iterations
             assert np.linalg.norm(np.maximum(x, 0) - want) <= 1e-12 * np.linalg.norm(want)
+
+
+def test_auto_order_rule():
+    """GraphIndex(reorder="auto"): small operators and hub-free graphs whose
+    given ids already keep neighbours close stay as they are; a hub-free graph
+    with scrambled ids gets RCM; power-law graphs get the degree-class order.
+    Any order is a permutation (the solve is order-invariant up to roundoff)."""
+    from paper_1912_06525_b200 import generators as G
+    from paper_1912_06525_b200.index import auto_order, degclass_rcm_order
+
+    small = G.config_graph("cfg1")
+    assert auto_order(small) is None  # under 10^6 stored entries
+    sbm, _ = G.sbm_split(n=80_000, seed=0)
+    assert sbm.nnz > 1_000_000
+    assert auto_order(sbm) is None  # community-contiguous ids beat RCM
+    rng = np.random.default_rng(0)
+    relabel = rng.permutation(sbm.n)
+    u = np.repeat(np.arange(sbm.n), np.diff(sbm.row_offsets))
+    scr = kz.from_edges(np.stack([relabel[u], relabel[sbm.col_indices]], axis=1))
+    o = auto_order(scr)
+    assert o is not None and np.array_equal(np.sort(o), np.arange(scr.n))
+    rmat = G.rmat_graph(16)
+    assert np.array_equal(auto_order(rmat), degclass_rcm_order(rmat))
