@@ -90,7 +90,8 @@ int kz_graph_info(const kz_graph* g, int64_t* rows, int64_t* cols, int64_t* nnz,
  * Y = s0*Z + s1*Xs + s2*(A Xg)  on b columns in layout [b/C][.][C];
  * Xg has `cols` rows, Xs/Z/Y/D have `rows` rows.  Z or Xs may be NULL.
  * If dots != NULL (device double[b]) it receives dots[j] = sum_i D[i,j]*Y[i,j]
- * (D == NULL means D = Xs).  Replaces KatzIndex.apply_m_permuted
+ * (D == NULL means D = Xs; dots need chunk <= 32, chunk 64 computes the
+ * product only).  Replaces KatzIndex.apply_m_permuted
  * (index.py:86-91) with s0=0, s1=1, s2=-alpha, and the m12 / m12.T products
  * of solver.py:110,115,178.  Workspace: kz_spmm_workspace_bytes(). */
 size_t kz_spmm_workspace_bytes(const kz_graph* g, int32_t b, int32_t chunk);

@@ -490,6 +490,8 @@ extern "C" int kz_spmm(const kz_graph* g, int32_t b, int32_t chunk, const double
         return fail(KZ_EARG, "b must be a positive multiple of the chunk width (1,2,4,...,32)");
     if (!Xg || !Y) return fail(KZ_EARG, "NULL X or Y");
     if (dots && !D && !Xs) return fail(KZ_EARG, "dots need D or Xs");
+    // the column-dot reduction maps one lane to one column of the chunk
+    if (dots && chunk > 32) return fail(KZ_EARG, "dots need a chunk width of at most 32");
     if (Xs && g->rows != g->cols) {
         // allowed: Xs simply has `rows` rows
     }

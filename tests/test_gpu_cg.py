@@ -90,6 +90,25 @@ def test_spmm_matches_scipy(torch, kz, graph, b, C):
     assert torch.equal(Yd, Y2)
 
 
+def test_spmm_chunk64_products_and_dot_guard(torch, kz):
+    """Chunk width 64 (512-byte rows) is a valid K1 width for the product;
+    the fused column dots map one lane to one column of a chunk, so they are
+    refused above 32 with a clear error instead of returning partial dots."""
+    rec, n = chunglu_fixture()
+    off, col = rec["row_offsets"], rec["col_indices"]
+    a = O.csr_matrix(off, col, n)
+    op = kz.DeviceOperator(off, col.astype(np.int32), n)
+    X = np.random.default_rng(64).standard_normal((n, 64))
+    Xd = torch.as_tensor(to_blk(X, 64)).cuda()
+    Yd = torch.empty_like(Xd)
+    op.spmm(Xd, Yd, b=64, chunk=64, Xs=Xd, s1=1.0, s2=-0.013)
+    want = X - 0.013 * (a @ X)
+    assert np.abs(from_blk(Yd.cpu().numpy(), n, 64, 64) - want).max() <= 1e-13 * np.abs(want).max()
+    dots = torch.empty(64, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="chunk width of at most 32"):
+        op.spmm(Xd, Yd, b=64, chunk=64, Xs=Xd, s1=1.0, s2=-0.013, dots=dots)
+
+
 @pytest.mark.parametrize("slice_mb,min_deg", [(0.002, 40), (0.01, 128), (0.002, 1024)])
 def test_spmm_column_blocked_schedule(torch, kz, monkeypatch, slice_mb, min_deg):
     """The opt-in column-blocked long-row schedule of K1 (graph.cu SchedOpts,
