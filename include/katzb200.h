@@ -162,7 +162,7 @@ typedef struct kz_lrc_desc {
  * out[j][n2], recursive residual in the report. */
 typedef struct kz_lrc_args {
     int32_t b;
-    int32_t chunk; /* 0: default */
+    int32_t chunk; /* 0: default; 1, 2, 4, ..., 32 */
     int32_t clamp;
     int32_t _pad;
     const int64_t* qpos; /* host int64[b] */

@@ -328,7 +328,8 @@ extern "C" int kz_lrc_batch(const kz_lrc* h, const kz_lrc_args* a, void* ws, siz
     if (!h->spectrum_ok) return fail(KZ_ESPECTRUM, "correction eigenvalue at or above 1");
     const int b = a->b;
     const int C = lrc_chunk(a);
-    if (!chunk_ok(C)) return fail(KZ_EARG, "bad chunk width");
+    // the PCG dots are fused into K1, whose reduction covers chunks of at most 32 columns
+    if (!chunk_ok(C) || C > 32) return fail(KZ_EARG, "bad chunk width");
     if (!ws || ws_bytes < kz_lrc_workspace_bytes(h, b, C)) return fail(KZ_EARG, "workspace too small");
     const int64_t n = h->n, n1 = h->n1, n2 = h->n2;
     if (!mode_pcg)
