@@ -333,7 +333,10 @@ def main():
     if world > 1:
         dist.barrier()
     first = len(clocks.rows)
+    # ncu --profile-from-start off captures exactly the timed steps (no-ops otherwise)
+    torch.cuda.cudart().cudaProfilerStart()
     ms, reps_all, launches, k1_ms, k1_n = timed(head, args.steps, k1=True)
+    torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
         dist.barrier()
     # a short timed region (cfg1/cfg2) ends before the 200 ms sampling
