@@ -370,6 +370,7 @@ struct SpmmArgs {
     int32_t nsuper;     // super groups per chunk
     int32_t super_size; // groups per super group (spmm_super_size)
     int32_t nchunks;
+    int32_t chunk0;     // first chunk of this launch (0 unless the SpMM is launched chunk by chunk)
     int32_t nwarps;     // warps of the (persistent) launch
     const double* Xg;
     const double* Xs;
@@ -501,7 +502,8 @@ __global__ void __launch_bounds__(kThreads, kSpmmMinBlocks) spmm_kernel(SpmmArgs
         if (lane == 0) g = atomicAdd(a.queue, 1);
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= total) break;
-        const int chunk = g / a.ngroups, gl = g - chunk * a.ngroups;
+        const int cq = g / a.ngroups, gl = g - cq * a.ngroups;
+        const int chunk = a.chunk0 + cq;  // chunk0 > 0: per-chunk launches (KZ_K1_L2WINDOW_ROWS experiment)
         if (a.chunk_active && !a.chunk_active[chunk]) continue;
         const double* __restrict__ Xc = a.Xg + static_cast<size_t>(chunk) * a.ldxg;
         // wide chunks (32-byte gathers): the column-dot accumulators live in
@@ -821,6 +823,47 @@ inline int launch_spmm(const kz_graph* g, int C, int nchunks, SpmmArgs a, cudaSt
         const char* e = std::getenv("KZ_K1_CARVEOUT");
         return e ? std::atoi(e) : -1;
     }();
+    // experiment: one launch per chunk with an L2 persisting
+    // access-policy window over the chunk's first KZ_K1_L2WINDOW_ROWS rows of Xg
+    // (the hub rows in the degree-class order); KZ_K1_L2WINDOW_MB = set-aside size
+    static const int win_rows = [] {
+        const char* e = std::getenv("KZ_K1_L2WINDOW_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (win_rows > 0 && C == 32 && !w && nchunks > 1 && a.chunk0 == 0 && !tev) {
+        static const bool set_aside = [] {
+            const char* e = std::getenv("KZ_K1_L2WINDOW_MB");
+            const size_t mb = e ? std::atoi(e) : 40;
+            return cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, mb << 20) == cudaSuccess;
+        }();
+        (void)set_aside;
+        static const float hit_ratio = [] {
+            const char* e = std::getenv("KZ_K1_L2WINDOW_HIT");
+            return e ? static_cast<float>(std::atof(e)) : 1.0f;
+        }();
+        for (int c = 0; c < nchunks; ++c) {
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = const_cast<double*>(a.Xg) + static_cast<size_t>(c) * a.ldxg;
+            attr.accessPolicyWindow.num_bytes = static_cast<size_t>(std::min<int64_t>(win_rows, g->cols)) * C * sizeof(double);
+            attr.accessPolicyWindow.hitRatio = hit_ratio;
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr);
+            SpmmArgs ac = a;
+            ac.chunk0 = c;
+            ac.nchunks = 1;
+            const int64_t tot1 = a.ngroups;
+            const unsigned grid1 = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cap, (tot1 + kWarps - 1) / kWarps)));
+            ac.nwarps = static_cast<int32_t>(grid1) * kWarps;
+            spmm_kernel<32, false><<<grid1, kThreads, 0, st>>>(ac);
+            note_launch();
+        }
+        cudaStreamAttrValue off{};
+        off.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &off);
+        KZ_LAUNCH_CHECK();
+        return KZ_OK;
+    }
 #define KZ_SPMM_CASE(CC)                                                                  \
     case CC:                                                                              \
         if (carveout >= 0) {                                                              \
