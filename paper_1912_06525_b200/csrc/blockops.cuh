@@ -518,6 +518,23 @@ __global__ void scatter_rhs_kernel(double* __restrict__ r, int64_t ld,
         r[static_cast<size_t>(j / C) * ld + static_cast<size_t>(colidx[k]) * C + (j % C)] = beta;
 }
 
+// ||b||^2 of the rhs columns scatter_rhs_kernel wrote, in closed form: b has
+// deg(q_j) entries equal to beta (binary operator), so ||b||^2 = beta^2 deg(q_j)
+// -- the norm solver.py:71-72 takes of the same vector, without a pass over the
+// block -- followed by the init finalize for r == b.  One CTA per chunk.
+template <int C>
+__global__ void rhs_norm_init_kernel(SolveState s, const int32_t* __restrict__ rowptr,
+                                     const int64_t* __restrict__ qpos, double beta) {
+    const int chunk = blockIdx.x;
+    const int col = chunk * C + threadIdx.x;
+    double v = 0.0;
+    if (threadIdx.x < C && col < s.b) {
+        const int64_t q = qpos[col];
+        v = __dmul_rn(__dmul_rn(beta, beta), static_cast<double>(rowptr[q + 1] - rowptr[q]));
+    }
+    finalize_chunk<C>(FIN_INIT_BR, s, nullptr, chunk, 0, v);
+}
+
 // column-major [b][rows] -> chunked block (tile transpose through shared memory)
 template <int C>
 __global__ void load_colmajor_kernel(double* __restrict__ dst, const double* __restrict__ src,

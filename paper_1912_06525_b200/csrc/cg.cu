@@ -277,9 +277,14 @@ static int cg_batch_impl(const kz_graph* g, const kz_cg_args* a, void* ws, size_
     KZ_LAUNCH_CHECK();
     // ||b||, optional start vector (solver.py:51-59), init finalize
     if (!eig) {
-        KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red,
-                                                                         a->x0 ? FIN_INIT_B : FIN_INIT_BR,
-                                                                         s, nullptr, 0); ::kz::note_launch());
+        if (!a->rhs && !a->x0 && !g->vals) {
+            // rhs = beta A e_q on a binary operator: ||b||^2 = beta^2 deg(q) needs no pass over the block
+            KZ_DISPATCH_C(C, rhs_norm_init_kernel<CC><<<nchunks, CC < 32 ? 32 : CC, 0, st>>>(s, g->rowptr, w.qpos, a->beta); ::kz::note_launch());
+        } else {
+            KZ_DISPATCH_C(C, coldot_kernel<CC><<<sgrid, kThreads, 0, st>>>(w.r, w.r, n, n * CC, n * CC, w.red,
+                                                                             a->x0 ? FIN_INIT_B : FIN_INIT_BR,
+                                                                             s, nullptr, 0); ::kz::note_launch());
+        }
         KZ_LAUNCH_CHECK();
     }
     if (a->x0) {
