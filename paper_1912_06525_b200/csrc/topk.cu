@@ -124,10 +124,22 @@ __global__ void __launch_bounds__(kThreads)
     const double* col = scores + static_cast<size_t>(j) * n;
     const int64_t per = (n + slices - 1) / slices;
     const int64_t i0 = sl * per, i1 = (n < i0 + per ? n : i0 + per);
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
-        const unsigned long long hi = score_key(col[i]);
-        const unsigned int lo = ~static_cast<unsigned int>(i);
-        if (cmp_prefix(hi, lo, c, c.shift) == 0 && !above_bound(m, j, hi, lo)) atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
+    // 4 loads in flight per thread: the scan streams the whole score block
+    for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += 4 * kThreads) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = ib + static_cast<int64_t>(u) * kThreads;
+            v[u] = i < i1 ? col[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = ib + static_cast<int64_t>(u) * kThreads;
+            if (i >= i1) break;
+            const unsigned long long hi = score_key(v[u]);
+            const unsigned int lo = ~static_cast<unsigned int>(i);
+            if (cmp_prefix(hi, lo, c, c.shift) == 0 && !above_bound(m, j, hi, lo)) atomicAdd(&h[digit_of(hi, lo, ns)], 1u);
+        }
     }
     __syncthreads();
     unsigned int* gh = hist + static_cast<size_t>(j) * kBins;
@@ -232,14 +244,25 @@ __global__ void __launch_bounds__(kThreads)
     const double* col = scores + static_cast<size_t>(j) * n;
     const int64_t per = (n + slices - 1) / slices;
     const int64_t i0 = sl * per, i1 = (n < i0 + per ? n : i0 + per);
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += kThreads) {
-        const unsigned long long hi = score_key(col[i]);
-        const unsigned int lo = ~static_cast<unsigned int>(i);
-        if (cmp_prefix(hi, lo, c, c.shift) >= 0 && !above_bound(m, j, hi, lo) && !is_masked(m, j, i)) {
-            const int pos = atomicAdd(&cs[j].ncand, 1);
-            if (pos < kCap) {
-                ckey[static_cast<size_t>(j) * kCap + pos] = hi;
-                cid[static_cast<size_t>(j) * kCap + pos] = static_cast<int>(i);
+    for (int64_t ib = i0 + threadIdx.x; ib < i1; ib += 4 * kThreads) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = ib + static_cast<int64_t>(u) * kThreads;
+            v[u] = i < i1 ? col[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = ib + static_cast<int64_t>(u) * kThreads;
+            if (i >= i1) break;
+            const unsigned long long hi = score_key(v[u]);
+            const unsigned int lo = ~static_cast<unsigned int>(i);
+            if (cmp_prefix(hi, lo, c, c.shift) >= 0 && !above_bound(m, j, hi, lo) && !is_masked(m, j, i)) {
+                const int pos = atomicAdd(&cs[j].ncand, 1);
+                if (pos < kCap) {
+                    ckey[static_cast<size_t>(j) * kCap + pos] = hi;
+                    cid[static_cast<size_t>(j) * kCap + pos] = static_cast<int>(i);
+                }
             }
         }
     }
