@@ -201,6 +201,12 @@ __global__ void __launch_bounds__(kSmallCgThreads, kSmallCgCtasPerSm) cg_small_k
     }
     __syncthreads();
     auto chunk_flags = [&]() {
+        // phase 3's x / p update still reads s_chunk: no thread may rewrite the
+        // flags before every warp of the CTA has left that loop (without this
+        // barrier a fast warp could clear a chunk's flag -- its last column
+        // just converged -- while slower warps had not started that chunk, and
+        // their rows of x missed the final update; found by tools/fuzz_parity.py)
+        __syncthreads();
         if (threadIdx.x < nch) {
             int any = 0;
             for (int c = 0; c < C; ++c) any |= s_act[threadIdx.x * C + c];

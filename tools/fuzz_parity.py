@@ -1,0 +1,137 @@
+"""Randomised parity sweep of the GPU query path against the CPU oracle
+(not part of the test suite: ~100 random cases in a few minutes on one GPU).
+
+Each case draws a random connected graph (Erdos-Renyi, preferential
+attachment with a few very high-degree hubs, star-of-cliques, path-like),
+a damping factor beta*lambda in (0.05, 0.97), a batch size that is or is not
+a multiple of the chunk width, a tolerance, a solve order, and checks
+  * query_cg_baseline_batch: iterations within +/-1 of oracle.query_cg_csr,
+    scores within 1e-10 relative L2 (plus the reach of one extra iteration),
+  * katz_rank_batch: the oracle's candidate order apart from keys tied
+    within 1e-12 of the column norm,
+  * sparse_katz_batch (every 4th case): same candidates, correlations within
+    1e-8.
+python tools/fuzz_parity.py [--cases 100] [--seed 0]"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+
+import paper_1912_06525_b200 as kz
+from oracle import katz_oracle as O
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cases", type=int, default=100)
+ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--only", type=int, default=-1, help="replay one case of the sequence (verbose)")
+a = ap.parse_args()
+rng = np.random.default_rng(a.seed)
+
+
+def random_edges(kind, n):
+    if kind == "er":
+        m = int(n * rng.uniform(1.5, 6.0))
+        e = rng.integers(0, n, size=(m, 2))
+    elif kind == "hubs":  # preferential-ish: a few hubs wired to most nodes (long rows: > 4096 entries when n allows)
+        hubs = rng.choice(n, size=max(1, n // int(rng.choice([400, 4000]))), replace=False)
+        e1 = np.stack([rng.choice(hubs, size=3 * n), rng.integers(0, n, size=3 * n)], axis=1)
+        e2 = rng.integers(0, n, size=(n, 2))
+        e = np.concatenate([e1, e2])
+    elif kind == "cliques":
+        k = int(rng.integers(3, 12))
+        blocks = n // k
+        u = np.repeat(np.arange(blocks * k), k)
+        v = (u // k) * k + np.tile(np.arange(k), blocks * k)
+        e = np.concatenate([np.stack([u, v], axis=1), rng.integers(0, n, size=(blocks, 2))])
+    else:  # path with chords
+        u = np.arange(n - 1)
+        e = np.concatenate([np.stack([u, u + 1], axis=1), rng.integers(0, n, size=(n // 5 + 1, 2))])
+    return e
+
+
+fails = 0
+for case in range(a.cases):
+    kind = ["er", "hubs", "cliques", "path"][case % 4]
+    n0 = int(rng.choice([40, 300, 2000, 9000, 30000, 60000]))
+    edges = random_edges(kind, n0)
+    skip = a.only >= 0 and case != a.only
+    g = kz.largest_connected_component(kz.from_edges(edges))
+    if g.n < 8:
+        continue
+    am = O.csr_matrix(g.row_offsets, g.col_indices, g.n)
+    lam = O.spectral_norm(am) if not skip else 1.0
+    beta = float(rng.uniform(0.05, 0.97)) / lam
+    tol = float(rng.choice([1e-6, 1e-8, 1e-10]))
+    b = int(rng.choice([1, 3, 16, 33, 64, 70]))
+    b = min(b, g.n)
+    reorder = str(rng.choice(["auto", "none", "rcm", "degclass"]))
+    qs = rng.choice(g.original_ids, size=b, replace=False)
+    if skip:
+        rng.choice([1, 5, 50])  # the s_rank draw of the skipped case
+        continue
+    idx = kz.GraphIndex(g, beta, spectral_norm=lam, reorder=reorder)
+    internal = idx.internal_ids(qs)
+    tag = {"case": case, "kind": kind, "n": int(g.n), "nnz": int(g.nnz), "max_deg": int(np.diff(g.row_offsets).max()),
+           "beta_lambda": round(beta * lam, 3), "tol": tol, "b": b, "reorder": reorder}
+    try:
+        scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol)
+        scores = np.asarray(scores)
+        s_rank = int(min(rng.choice([1, 5, 50]), g.n - 1))
+        ranked = kz.katz_rank_batch(idx, qs, s_rank, tol=tol)
+        bad = []
+        for j in range(b):
+            want, wrep = O.query_cg_csr(am, beta, int(internal[j]), tol=tol)
+            if a.only >= 0:
+                print(json.dumps({"col": j, "q": int(qs[j]), "deg": int(am.indptr[internal[j] + 1] - am.indptr[internal[j]]),
+                                  "it_gpu": int(reps[j].iterations), "it_ref": int(wrep.iterations),
+                                  "res_gpu": float(reps[j].final_residual_norm), "res_ref": float(wrep.final_residual_norm),
+                                  "conv_gpu": bool(reps[j].converged), "conv_ref": bool(wrep.converged),
+                                  "err": float(np.linalg.norm(scores[j] - want) / np.linalg.norm(want))}), flush=True)
+            if abs(int(reps[j].iterations) - int(wrep.iterations)) > 1:
+                bad.append(("iterations", j, int(reps[j].iterations), int(wrep.iterations)))
+            # one iteration of slack moves the answer by at most ~tol*|b|*cond
+            slack = 1e-10 if reps[j].iterations == wrep.iterations else 10 * tol
+            err = np.linalg.norm(scores[j] - want) / np.linalg.norm(want)
+            if err > slack:
+                bad.append(("scores", j, float(err)))
+            nb = am.indices[am.indptr[internal[j]]: am.indptr[internal[j] + 1]]
+            order = O.candidate_order(g.n, scores[j], int(internal[j]), nb, s_rank)
+            got = np.array([c for c, _ in ranked[j].candidates])
+            wid = np.asarray(g.original_ids)[order]
+            if len(got) != len(wid):
+                bad.append(("rank length", j, len(got), len(wid)))
+            else:
+                diff = np.flatnonzero(got != wid)
+                pos = {int(o): i for i, o in enumerate(np.asarray(g.original_ids))}
+                nx = np.linalg.norm(scores[j])
+                for d in diff:
+                    if abs(scores[j][pos[int(got[d])]] - scores[j][pos[int(wid[d])]]) > 1e-12 * nx:
+                        bad.append(("rank order", j, int(d)))
+                        break
+        if case % 4 == 0 and g.n > 30:
+            s = int(min(6, g.n - 2))
+            q3 = qs[: min(3, b)]
+            preds = kz.sparse_katz_batch(idx, q3, s, tol=1e-10)
+            solve = lambda i: O.query_cg_csr(am, beta, int(i), tol=1e-10)[0]  # noqa: E731
+            nbrs = lambda i: am.indices[am.indptr[i]: am.indptr[i + 1]]  # noqa: E731
+            for j, q in enumerate(q3):
+                want = O.sparse_katz(solve, nbrs, g.original_ids, int(idx.internal_ids([q])[0]), s)
+                gotc = preds[j].candidates
+                wc = dict(want)
+                if sorted(c for c, _ in gotc) != sorted(c for c, _ in want):
+                    bad.append(("sparse_katz set", j))
+                elif any(abs(r - wc[c]) > 1e-8 for c, r in gotc):
+                    bad.append(("sparse_katz corr", j))
+        if bad:
+            fails += 1
+            print(json.dumps({**tag, "FAIL": bad[:4]}), flush=True)
+        else:
+            print(json.dumps({**tag, "ok": True}), flush=True)
+    except Exception as ex:  # noqa: BLE001
+        fails += 1
+        print(json.dumps({**tag, "EXCEPTION": repr(ex)[:300]}), flush=True)
+print(json.dumps({"cases": a.cases, "failures": fails}))
