@@ -28,6 +28,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cases", type=int, default=100)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--only", type=int, default=-1, help="replay one case of the sequence (verbose)")
+ap.add_argument("--dump", default=None, help="with --only: save the case (CSR, queries, beta, tol) as .npz")
 a = ap.parse_args()
 rng = np.random.default_rng(a.seed)
 
@@ -73,6 +74,9 @@ for case in range(a.cases):
     if skip:
         rng.choice([1, 5, 50])  # the s_rank draw of the skipped case
         continue
+    if a.dump:
+        np.savez_compressed(a.dump, row_offsets=g.row_offsets, col_indices=g.col_indices.astype(np.int32),
+                            original_ids=g.original_ids, queries=qs, beta=beta, lam=lam, tol=tol, reorder=reorder)
     idx = kz.GraphIndex(g, beta, spectral_norm=lam, reorder=reorder)
     internal = idx.internal_ids(qs)
     tag = {"case": case, "kind": kind, "n": int(g.n), "nnz": int(g.nnz), "max_deg": int(np.diff(g.row_offsets).max()),
