@@ -10,7 +10,9 @@ a multiple of the chunk width, a tolerance, a solve order, and checks
   * katz_rank_batch: the oracle's candidate order apart from keys tied
     within 1e-12 of the column norm,
   * sparse_katz_batch (every 4th case): same candidates, correlations within
-    1e-8.
+    1e-8,
+  * LRC-Katz (every 8th case, n <= 4000): build_index on the device, the saved
+    KLRC bytes read by the oracle, query_batch against oracle.query_lrc.
 python tools/fuzz_parity.py [--cases 100] [--seed 0]"""
 import argparse
 import json
@@ -58,6 +60,9 @@ fails = 0
 for case in range(a.cases):
     kind = ["er", "hubs", "cliques", "path"][case % 4]
     n0 = int(rng.choice([40, 300, 2000, 9000, 30000, 60000]))
+    big = case % 10 == 7  # mid-size solves: the graph-replayed and host-driven loops
+    if big:
+        n0 = int(rng.choice([150000, 400000]))
     edges = random_edges(kind, n0)
     skip = a.only >= 0 and case != a.only
     g = kz.largest_connected_component(kz.from_edges(edges))
@@ -68,11 +73,17 @@ for case in range(a.cases):
     beta = float(rng.uniform(0.05, 0.97)) / lam
     tol = float(rng.choice([1e-6, 1e-8, 1e-10]))
     b = int(rng.choice([1, 3, 16, 33, 64, 70]))
+    if big:
+        b = int(rng.choice([64, 200, 256]))
     b = min(b, g.n)
+    start_seed = int(rng.integers(0, 1000)) if case % 5 == 3 else None
+    max_iter = int(rng.integers(1, 5)) if case % 7 == 5 else None
     reorder = str(rng.choice(["auto", "none", "rcm", "degclass"]))
     qs = rng.choice(g.original_ids, size=b, replace=False)
     if skip:
         rng.choice([1, 5, 50])  # the s_rank draw of the skipped case
+        if big:
+            rng.choice(b, size=min(b, 6), replace=False)
         continue
     if a.dump:
         np.savez_compressed(a.dump, row_offsets=g.row_offsets, col_indices=g.col_indices.astype(np.int32),
@@ -82,13 +93,18 @@ for case in range(a.cases):
     tag = {"case": case, "kind": kind, "n": int(g.n), "nnz": int(g.nnz), "max_deg": int(np.diff(g.row_offsets).max()),
            "beta_lambda": round(beta * lam, 3), "tol": tol, "b": b, "reorder": reorder}
     try:
-        scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol)
+        scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol, start_seed=start_seed, max_iter=max_iter)
         scores = np.asarray(scores)
         s_rank = int(min(rng.choice([1, 5, 50]), g.n - 1))
         ranked = kz.katz_rank_batch(idx, qs, s_rank, tol=tol)
+        plain = start_seed is None and max_iter is None  # katz_rank solves from zero with the default budget
+        cols = range(b) if not big else rng.choice(b, size=min(b, 6), replace=False)
+        tag.update(start_seed=start_seed, max_iter=max_iter)
         bad = []
-        for j in range(b):
-            want, wrep = O.query_cg_csr(am, beta, int(internal[j]), tol=tol)
+        for j in cols:
+            want, wrep = O.query_cg_csr(am, beta, int(internal[j]), tol=tol, start_seed=start_seed, max_iter=max_iter)
+            if bool(reps[j].converged) != bool(wrep.converged) and abs(int(reps[j].iterations) - int(wrep.iterations)) == 0:
+                bad.append(("converged flag", int(j)))
             if a.only >= 0:
                 print(json.dumps({"col": j, "q": int(qs[j]), "deg": int(am.indptr[internal[j] + 1] - am.indptr[internal[j]]),
                                   "it_gpu": int(reps[j].iterations), "it_ref": int(wrep.iterations),
@@ -102,6 +118,8 @@ for case in range(a.cases):
             err = np.linalg.norm(scores[j] - want) / np.linalg.norm(want)
             if err > slack:
                 bad.append(("scores", j, float(err)))
+            if not plain:
+                continue
             nb = am.indices[am.indptr[internal[j]]: am.indptr[internal[j] + 1]]
             order = O.candidate_order(g.n, scores[j], int(internal[j]), nb, s_rank)
             got = np.array([c for c, _ in ranked[j].candidates])
@@ -130,6 +148,28 @@ for case in range(a.cases):
                     bad.append(("sparse_katz set", j))
                 elif any(abs(r - wc[c]) > 1e-8 for c, r in gotc):
                     bad.append(("sparse_katz corr", j))
+        # LRC-Katz on a device-built index (every 8th case, small graphs): the
+        # saved KLRC bytes go to the oracle's reader, whose Schur PCG is the pin
+        if case % 8 == 1 and 60 <= g.n <= 4000:
+            import io
+
+            ell = int(min(rng.choice([4, 16, 32]), max(2, g.n // 8)))
+            lidx = kz.build_index(g, alpha=beta, ell=ell, seed=0, spectral_norm=lam)
+            buf = io.BytesIO()
+            kz.save_index(lidx, buf)
+            oix = O.read_klrc(buf.getvalue())
+            q4 = qs[: min(4, b)]
+            lsc, lrep = kz.query_batch(lidx, q4, tol=tol)
+            lsc = np.asarray(lsc)
+            for j, q in enumerate(q4):
+                want, wrep = O.query_lrc(oix, int(q), tol=tol)
+                if abs(int(lrep[j].iterations) - int(wrep.iterations)) > 1:
+                    bad.append(("lrc iterations", j, int(lrep[j].iterations), int(wrep.iterations)))
+                slack = 1e-10 if lrep[j].iterations == wrep.iterations else 10 * tol
+                err = np.linalg.norm(lsc[j] - want) / np.linalg.norm(want)
+                if err > slack:
+                    bad.append(("lrc scores", j, float(err)))
+            tag["lrc_ell"] = ell
         if bad:
             fails += 1
             print(json.dumps({**tag, "FAIL": bad[:4]}), flush=True)
