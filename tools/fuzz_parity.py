@@ -12,7 +12,11 @@ a multiple of the chunk width, a tolerance, a solve order, and checks
   * sparse_katz_batch (every 4th case): same candidates, correlations within
     1e-8,
   * LRC-Katz (every 8th case, n <= 4000): build_index on the device, the saved
-    KLRC bytes read by the oracle, query_batch against oracle.query_lrc.
+    KLRC bytes read by the oracle, query_batch against oracle.query_lrc,
+  * from_edges_device against from_edges (every case, byte-identical CSR),
+  * the eigen form (every 6th case; rank 4-48, 0-3 walk terms) against the exact
+    solution within 4 * cond * tol,
+  * katz_rank_batch with s = 5,000 (every 9th case: two top-k passes).
 python tools/fuzz_parity.py [--cases 100] [--seed 0]"""
 import argparse
 import json
@@ -148,6 +152,46 @@ for case in range(a.cases):
                     bad.append(("sparse_katz set", j))
                 elif any(abs(r - wc[c]) > 1e-8 for c, r in gotc):
                     bad.append(("sparse_katz corr", j))
+        # ingestion: the device from_edges gives the host CSR byte for byte
+        gd, _ = kz.from_edges_device(edges[:, 0], edges[:, 1], n0)
+        gh = kz.from_edges(edges, n=n0)
+        if not (np.array_equal(gd.row_offsets, gh.row_offsets) and np.array_equal(gd.col_indices, gh.col_indices)):
+            bad.append(("from_edges_device",))
+        # eigen-form start (every 6th case): rank and walk terms drawn; against the
+        # exact solution (oracle CG at 1e-13) within cond * tol
+        if case % 6 == 2 and g.n >= 500 and plain:
+            rank = int(rng.choice([4, 16, 48]))
+            wt = int(rng.choice([0, 1, 2, 3]))
+            ei = kz.EigenIndex(idx, rank, walk_terms=wt)
+            q4 = qs[: min(4, b)]
+            esc, erep = kz.query_batch(ei, q4, tol=tol)
+            esc = np.asarray(esc)
+            cond = (1.0 + beta * lam) / (1.0 - beta * lam)
+            for j in range(len(q4)):
+                exact, _ = O.query_cg_csr(am, beta, int(internal[j]), tol=1e-13)
+                err = np.linalg.norm(esc[j] - exact) / np.linalg.norm(exact)
+                if err > 4.0 * cond * tol:
+                    bad.append(("eigen scores", j, float(err), rank, wt))
+            tag["eigen"] = [rank, wt]
+        # a top-k deeper than one 4,096-entry pass (every 9th case)
+        if case % 9 == 4 and g.n >= 9000 and plain:
+            deep = kz.katz_rank_batch(idx, qs[:2], 5000, tol=tol)
+            for j in range(min(2, b)):
+                nb = am.indices[am.indptr[internal[j]]: am.indptr[internal[j] + 1]]
+                order = O.candidate_order(g.n, scores[j], int(internal[j]), nb, 5000)
+                got = np.array([c for c, _ in deep[j].candidates])
+                wid = np.asarray(g.original_ids)[order]
+                if len(got) != len(wid):
+                    bad.append(("deep rank length", j, len(got), len(wid)))
+                else:
+                    diff = np.flatnonzero(got != wid)
+                    if diff.size:
+                        pos = np.empty(int(np.asarray(g.original_ids).max()) + 1, dtype=np.int64)
+                        pos[np.asarray(g.original_ids)] = np.arange(g.n)
+                        gap = np.abs(scores[j][pos[got[diff]]] - scores[j][pos[wid[diff]]]).max()
+                        if gap > 1e-12 * np.linalg.norm(scores[j]):
+                            bad.append(("deep rank order", j, float(gap)))
+            tag["deep_k"] = 5000
         # LRC-Katz on a device-built index (every 8th case, small graphs): the
         # saved KLRC bytes go to the oracle's reader, whose Schur PCG is the pin
         if case % 8 == 1 and 60 <= g.n <= 4000:
