@@ -34,6 +34,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cases", type=int, default=100)
 ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--only", type=int, default=-1, help="replay one case of the sequence (verbose)")
+ap.add_argument("--focus", default=None, choices=[None, "lrc", "eigen"], help="every case exercises this path")
 ap.add_argument("--dump", default=None, help="with --only: save the case (CSR, queries, beta, tol) as .npz")
 a = ap.parse_args()
 rng = np.random.default_rng(a.seed)
@@ -64,7 +65,11 @@ fails = 0
 for case in range(a.cases):
     kind = ["er", "hubs", "cliques", "path"][case % 4]
     n0 = int(rng.choice([40, 300, 2000, 9000, 30000, 60000]))
-    big = case % 10 == 7  # mid-size solves: the graph-replayed and host-driven loops
+    if a.focus == "lrc":
+        n0 = int(rng.choice([300, 2000, 4000]))
+    elif a.focus == "eigen":
+        n0 = int(rng.choice([2000, 9000, 30000]))
+    big = case % 10 == 7 and a.focus is None  # mid-size solves: the graph-replayed and host-driven loops
     if big:
         n0 = int(rng.choice([150000, 400000]))
     edges = random_edges(kind, n0)
@@ -159,7 +164,7 @@ for case in range(a.cases):
             bad.append(("from_edges_device",))
         # eigen-form start (every 6th case): rank and walk terms drawn; against the
         # exact solution (oracle CG at 1e-13) within cond * tol
-        if case % 6 == 2 and g.n >= 500 and plain:
+        if (case % 6 == 2 or a.focus == "eigen") and g.n >= 500 and plain:
             rank = int(rng.choice([4, 16, 48]))
             wt = int(rng.choice([0, 1, 2, 3]))
             ei = kz.EigenIndex(idx, rank, walk_terms=wt)
@@ -194,7 +199,7 @@ for case in range(a.cases):
             tag["deep_k"] = 5000
         # LRC-Katz on a device-built index (every 8th case, small graphs): the
         # saved KLRC bytes go to the oracle's reader, whose Schur PCG is the pin
-        if case % 8 == 1 and 60 <= g.n <= 4000:
+        if (case % 8 == 1 or a.focus == "lrc") and 60 <= g.n <= 4000:
             import io
 
             ell = int(min(rng.choice([4, 16, 32]), max(2, g.n // 8)))
@@ -213,6 +218,27 @@ for case in range(a.cases):
                 err = np.linalg.norm(lsc[j] - want) / np.linalg.norm(want)
                 if err > slack:
                     bad.append(("lrc scores", j, float(err)))
+            # the factor-level API on the same index: Schur operator, its rhs,
+            # the preconditioner and the PCG on random vectors
+            if oix.n2 > 0:
+                v2 = rng.standard_normal(oix.n2)
+                g1, g2 = rng.standard_normal(oix.n1), rng.standard_normal(oix.n2)
+
+                def close(got, want, what, rtol=1e-11):
+                    e = np.linalg.norm(np.asarray(got) - want) / max(np.linalg.norm(want), 1e-300)
+                    if e > rtol:
+                        bad.append((what, float(e)))
+
+                close(kz.apply_schur(lidx, v2), O.apply_schur(oix, v2), "apply_schur")
+                close(kz.schur_rhs(lidx, g1, g2), O.schur_rhs(oix, g1, g2), "schur_rhs")
+                close(kz.apply_approx_schur_inverse(lidx.dc, lidx.lr, v2), O.apply_approx_schur_inverse(oix, v2),
+                      "apply_approx_schur_inverse", 1e-9)
+                xg, rg = kz.lrc_pcg(lidx, g2, tol=tol)
+                xo, ro = O.lrc_pcg(oix, g2, tol=tol)
+                if abs(int(rg.iterations) - int(ro.iterations)) > 1:
+                    bad.append(("lrc_pcg iterations", int(rg.iterations), int(ro.iterations)))
+                elif rg.iterations == ro.iterations:
+                    close(xg, xo, "lrc_pcg x", 1e-9)
             tag["lrc_ell"] = ell
         if bad:
             fails += 1
