@@ -93,6 +93,10 @@ for case in range(a.cases):
         rng.choice([1, 5, 50])  # the s_rank draw of the skipped case
         if big:
             rng.choice(b, size=min(b, 6), replace=False)
+        if case % 4 == 0 and g.n > 30:
+            if g.n <= 9000:
+                rng.choice([2, 6, 30])
+            rng.integers(0, 3)
         continue
     if a.dump:
         np.savez_compressed(a.dump, row_offsets=g.row_offsets, col_indices=g.col_indices.astype(np.int32),
@@ -144,13 +148,23 @@ for case in range(a.cases):
                         bad.append(("rank order", j, int(d)))
                         break
         if case % 4 == 0 and g.n > 30:
-            s = int(min(6, g.n - 2))
+            s = int(min(rng.choice([2, 6, 30]) if g.n <= 9000 else 6, g.n - 2))
+            T = [None, 3, s + 5][int(rng.integers(0, 3))]
+            if T is not None:
+                T = int(min(T, g.n - 1))
             q3 = qs[: min(3, b)]
-            preds = kz.sparse_katz_batch(idx, q3, s, tol=1e-10)
-            solve = lambda i: O.query_cg_csr(am, beta, int(i), tol=1e-10)[0]  # noqa: E731
+            preds = kz.sparse_katz_batch(idx, q3, s, T, tol=1e-10)
+            cache = {}
+
+            def solve(i):
+                if int(i) not in cache:
+                    cache[int(i)] = O.query_cg_csr(am, beta, int(i), tol=1e-10)[0]
+                return cache[int(i)]
+
             nbrs = lambda i: am.indices[am.indptr[i]: am.indptr[i + 1]]  # noqa: E731
+            tag["sparse_katz"] = [s, T]
             for j, q in enumerate(q3):
-                want = O.sparse_katz(solve, nbrs, g.original_ids, int(idx.internal_ids([q])[0]), s)
+                want = O.sparse_katz(solve, nbrs, g.original_ids, int(idx.internal_ids([q])[0]), s, T)
                 gotc = preds[j].candidates
                 wc = dict(want)
                 if sorted(c for c, _ in gotc) != sorted(c for c, _ in want):
