@@ -108,12 +108,18 @@ for case in range(a.cases):
     try:
         scores, reps = kz.query_cg_baseline_batch(idx, qs, tol=tol, start_seed=start_seed, max_iter=max_iter)
         scores = np.asarray(scores)
+        # determinism: a second solve is bit-identical (every reduction has a fixed order)
+        scores2, _ = kz.query_cg_baseline_batch(idx, qs, tol=tol, start_seed=start_seed, max_iter=max_iter)
+        rerun_equal = np.array_equal(scores, np.asarray(scores2))
+        del scores2
         s_rank = int(min(rng.choice([1, 5, 50]), g.n - 1))
         ranked = kz.katz_rank_batch(idx, qs, s_rank, tol=tol)
         plain = start_seed is None and max_iter is None  # katz_rank solves from zero with the default budget
         cols = range(b) if not big else rng.choice(b, size=min(b, 6), replace=False)
         tag.update(start_seed=start_seed, max_iter=max_iter)
         bad = []
+        if not rerun_equal:
+            bad.append(("rerun differs",))
         for j in cols:
             want, wrep = O.query_cg_csr(am, beta, int(internal[j]), tol=tol, start_seed=start_seed, max_iter=max_iter)
             if bool(reps[j].converged) != bool(wrep.converged) and abs(int(reps[j].iterations) - int(wrep.iterations)) == 0:
@@ -185,6 +191,8 @@ for case in range(a.cases):
             q4 = qs[: min(4, b)]
             esc, erep = kz.query_batch(ei, q4, tol=tol)
             esc = np.asarray(esc)
+            if not np.array_equal(esc, np.asarray(kz.query_batch(ei, q4, tol=tol)[0])):
+                bad.append(("eigen rerun differs",))
             cond = (1.0 + beta * lam) / (1.0 - beta * lam)
             for j in range(len(q4)):
                 exact, _ = O.query_cg_csr(am, beta, int(internal[j]), tol=1e-13)
@@ -224,6 +232,8 @@ for case in range(a.cases):
             q4 = qs[: min(4, b)]
             lsc, lrep = kz.query_batch(lidx, q4, tol=tol)
             lsc = np.asarray(lsc)
+            if not np.array_equal(lsc, np.asarray(kz.query_batch(lidx, q4, tol=tol)[0])):
+                bad.append(("lrc rerun differs",))
             for j, q in enumerate(q4):
                 want, wrep = O.query_lrc(oix, int(q), tol=tol)
                 if abs(int(lrep[j].iterations) - int(wrep.iterations)) > 1:
