@@ -82,6 +82,8 @@ for case in range(a.cases):
     lam = O.spectral_norm(am) if not skip else 1.0
     beta = float(rng.uniform(0.05, 0.97)) / lam
     tol = float(rng.choice([1e-6, 1e-8, 1e-10]))
+    if case % 13 == 9:
+        tol = float(rng.choice([2.0, 0.5, 1e-2]))  # stops at once / after the sparse first iteration / after two
     b = int(rng.choice([1, 3, 16, 33, 64, 70]))
     if big:
         b = int(rng.choice([64, 200, 256]))
@@ -282,6 +284,11 @@ for case in range(a.cases):
         else:
             print(json.dumps({**tag, "ok": True}), flush=True)
     except Exception as ex:  # noqa: BLE001
+        if whole and start_seed is not None and "positive definite" in repr(ex):
+            # the degenerate zero-rhs seeded start (see above) may also end in p.q <= 0, which both
+            # sides report as RuntimeError (solver.py:84-85); the batch call raises for the batch
+            print(json.dumps({**tag, "ok": True, "degenerate": "p.q <= 0 on a zero rhs from a seeded start"}), flush=True)
+            continue
         fails += 1
         print(json.dumps({**tag, "EXCEPTION": repr(ex)[:300]}), flush=True)
 print(json.dumps({"cases": a.cases, "failures": fails}))
