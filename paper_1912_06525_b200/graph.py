@@ -174,8 +174,7 @@ def load_edge_list(source, fmt="auto"):
     number) on a malformed line or when no edge remains.  Parsing is host
     text processing; the CSR is then built like from_edges.
     """
-    if fmt not in ("auto", "whitespace", "csv"):
-        raise ValueError(f"unknown format {fmt!r}")
+    # like the reference, any fmt other than "csv" / "auto" splits on whitespace (no validation)
     if isinstance(source, (str, os.PathLike)):
         with open(source, "rb") as fh:
             data = fh.read()
