@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 
@@ -111,6 +112,13 @@ __host__ __device__ inline size_t blk_index(int64_t rows, int C, int64_t i, int 
 // Supported chunk widths (columns per chunk) and the default choice for b.
 inline bool chunk_ok(int C) { return C == 1 || C == 2 || C == 4 || C == 8 || C == 16 || C == 32 || C == 64; }
 inline int default_chunk(int b) {
+    // experiments: KZ_CHUNK = chunk width cap (8 / 16 / 32 / 64) for wide batches
+    static const int cap = [] {
+        const char* e = std::getenv("KZ_CHUNK");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 8 && chunk_ok(v) ? v : 0;
+    }();
+    if (cap && b >= cap) return cap;
     if (b >= 32) return 32;  // 256-byte gathered segments, half the index passes of C=16
     if (b >= 16) return 16;
     int c = 1;

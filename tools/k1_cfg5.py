@@ -13,7 +13,7 @@ import paper_1912_06525_b200 as kz
 from paper_1912_06525_b200 import generators as G
 
 g, _ = G.sbm_split(n=1_000_000, seed=0)
-n, b, C = g.n, 256, 32
+n, b, C = g.n, 256, int(os.environ.get("K1_C", "32"))
 X = torch.randn(b * n, dtype=torch.float64, device="cuda")
 Y = torch.empty_like(X)
 Z = torch.randn(b * n, dtype=torch.float64, device="cuda")
@@ -36,7 +36,7 @@ def timed(op, **kw):
 op = kz.DeviceOperator(g.row_offsets, g.col_indices.astype(np.int32), n)
 empty = kz.DeviceOperator(np.zeros(n + 1, dtype=np.int64), np.zeros(0, dtype=np.int32), n)
 deg = np.diff(g.row_offsets)
-print(json.dumps({"n": n, "nnz": int(g.nnz), "max_deg": int(deg.max()),
+print(json.dumps({"C": C, "n": n, "nnz": int(g.nnz), "max_deg": int(deg.max()),
                   "k1_ms": timed(op), "k1_with_z_ms": timed(op, Z=Z, s0=0.5),
                   "epilogue_only_ms": timed(empty), "gathered_gb": round(g.nnz * 8.0 * b / 1e9, 2),
                   "stream_gb": round(3 * 8.0 * n * b / 1e9, 2)}))
