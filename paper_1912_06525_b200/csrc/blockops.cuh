@@ -440,7 +440,7 @@ struct CgHistory {
     int bpad = 0;
 };
 
-constexpr int kMaxHist = 8;  // residual-history slots (cg.cu caps H at this)
+constexpr int kMaxHist = 16;  // residual-history slots (cg.cu caps H at this)
 
 // element e (chunked offset) of column col (a fully unrolled, predicated
 // variant measured 57% slower in the output gather)

@@ -73,10 +73,10 @@ void carve_cg(Carver& cv, const kz_graph* g, int b, CgWork& w, const kz_eigen* e
     w.nb = stream_ctas_per_chunk(g->rows, w.C, w.nchunks);
     const size_t blk = static_cast<size_t>(w.bpad) * g->rows;
     // residual-history slots (see blockops.cuh CgHistory): up to
-    // KZ_CG_HISTORY (default 8) while the vector blocks stay under 64 GB
+    // KZ_CG_HISTORY (default 16: cfg5 at tol 1e-10 needs 14) while the vector blocks stay under 64 GB
     {
         const char* e = std::getenv("KZ_CG_HISTORY");
-        const int want = e ? std::atoi(e) : 8;
+        const int want = e ? std::atoi(e) : 16;
         const double blk_gb = static_cast<double>(blk) * 8.0 / 1e9;
         int h = static_cast<int>(std::min<double>(std::min(want, kMaxHist),
                                                   std::floor(64.0 / std::max(blk_gb, 1e-9)) - 3.0));

@@ -278,13 +278,13 @@ def test_cg_sparse_first_iteration_matches_dense(torch, kz, cfg, monkeypatch):
     assert np.all(diff <= 1e-12), diff.max()
 
 
-@pytest.mark.parametrize("tol", [1e-8, 1e-12])
-def test_cg_residual_history_matches_per_iteration_update(torch, kz, monkeypatch, tol):
+@pytest.mark.parametrize("tol,slots", [(1e-8, None), (1e-12, None), (1e-12, 8), (1e-12, 4), (1e-8, 3)])
+def test_cg_residual_history_matches_per_iteration_update(torch, kz, monkeypatch, tol, slots):
     """The residual-history form of the solution (x = x0 + sum c_i r_i,
     blockops.cuh CgHistory; folded into x when a solve outgrows its slots,
-    which tol 1e-12 forces) against the per-iteration x update
-    (KZ_CG_HISTORY=0): identical iteration counts, scores within roundoff,
-    for plain CG and the eigen form."""
+    which 8 / 4 / 3 slots force -- the default is up to 16) against the
+    per-iteration x update (KZ_CG_HISTORY=0): identical iteration counts,
+    scores within roundoff, for plain CG and the eigen form."""
     from paper_1912_06525_b200.generators import CONFIGS, config_graph, sample_queries
 
     g = config_graph("proxy16")
@@ -293,6 +293,8 @@ def test_cg_residual_history_matches_per_iteration_update(torch, kz, monkeypatch
     ei = kz.EigenIndex(gi, 16)
     qs = sample_queries(g.original_ids, 40, seed=2)
     for fn, idx in ((kz.query_cg_baseline_batch, gi), (kz.query_batch, ei)):
+        if slots is not None:
+            monkeypatch.setenv("KZ_CG_HISTORY", str(slots))
         s1, r1 = fn(idx, qs, tol=tol, device=True)
         monkeypatch.setenv("KZ_CG_HISTORY", "0")
         s0, r0 = fn(idx, qs, tol=tol, device=True)
