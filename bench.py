@@ -373,10 +373,13 @@ def main():
     peak, peak_src = peaks()
     blk = 8.0 * n * b
     if args.solver == "cg":
-        alg = sum(k1_algorithmic_bytes(n, nnz, C, nch, it)[0] for it in iters_all)
+        per_solve = [k1_algorithmic_bytes(n, nnz, C, nch, it) for it in iters_all]
+        alg = sum(p[0] for p in per_solve)
+        k1_work = sum(p[1] for p in per_solve)
         alg_note = "sum over the timed steps of B_spmm per K1 launch with its active chunks"
     else:
         alg = (4.0 * nnz + 4.0 * (n + 1) + 2 * blk) * k1_n
+        k1_work = k1_n
         alg_note = "B_spmm at full width per K1 launch"
     achieved = alg / (k1_ms / 1e3) / 1e9 if k1_ms else None
     k1_share = k1_ms / (ms * args.steps) if k1_ms else None
@@ -455,7 +458,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "kernel": f"spmm_kernel<{C}> (K1)",
-                         "launch_ms": k1_ms / max(1, k1_n) if k1_ms else None, "launches_timed": k1_n,
+                         # launches with no active chunk (the iteration issued ahead of the
+                         # lagged stop poll) exit at once: the average is over working launches
+                         "launch_ms": k1_ms / max(1, min(k1_n, k1_work)) if k1_ms else None,
+                         "launches_timed": k1_n, "launches_with_work": min(k1_n, k1_work) if k1_n else None,
                          "k1_share_of_step": k1_share,
                          "algorithmic_bytes": alg, "algorithmic_note": alg_note,
                          "full_width_launch_alone_ms": spmm_alone_ms,
